@@ -1,0 +1,99 @@
+"""In-tree build of the native libraries (no JIT cache: the built .so files
+travel with the repo snapshot to the GPU box).
+
+* engine  : nvcc -gencode arch=compute_100a,code=sm_100a -> libsymmine_gpu.so
+* graph   : g++ -fopenmp                                  -> libsymmine_graph.so
+* oracle  : make -C oracle (test infrastructure: the C restatement always,
+            the reference library only when /root/reference is present)
+"""
+from __future__ import annotations
+
+import glob
+import os
+import shutil
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+ENGINE_SO = os.path.join(PKG, "libsymmine_gpu.so")
+GRAPH_SO = os.path.join(PKG, "libsymmine_graph.so")
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+REFERENCE = "/root/reference/proj"
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+    "--expt-relaxed-constexpr",
+]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: cannot build the CUDA engine")
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _engine_sources() -> list[str]:
+    return (sorted(glob.glob(os.path.join(CSRC, "*.cu"))) +
+            sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) +
+            [os.path.join(CSRC, "program.hpp"), os.path.join(INCLUDE, "symmine_gpu.h")])
+
+
+def build_engine(force: bool = False, verbose: bool = False) -> str:
+    srcs = _engine_sources()
+    if force or _stale(ENGINE_SO, srcs):
+        cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+        tmp = ENGINE_SO + ".tmp"
+        cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp, *cu]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, ENGINE_SO)
+    return ENGINE_SO
+
+
+def build_graph_lib(force: bool = False) -> str:
+    src = os.path.join(CSRC, "graphgen.cpp")
+    if force or _stale(GRAPH_SO, [src, os.path.join(INCLUDE, "symmine_graph.h")]):
+        tmp = GRAPH_SO + ".tmp"
+        subprocess.run(["g++", "-O3", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-Wall",
+                        "-o", tmp, src], check=True)
+        os.replace(tmp, GRAPH_SO)
+    return GRAPH_SO
+
+
+def build_oracle(reference: bool | None = None) -> None:
+    """Checker libraries (test infrastructure only)."""
+    subprocess.run(["make", "-s", "-C", ORACLE_DIR, "port"], check=True)
+    if reference is None:
+        reference = os.path.isdir(REFERENCE)
+    if reference:
+        subprocess.run(["make", "-s", "-j8", "-C", ORACLE_DIR, "ref"], check=True)
+
+
+def ensure_engine() -> str:
+    if not os.path.exists(ENGINE_SO):
+        build_engine()
+    return ENGINE_SO
+
+
+def ensure_graph_lib() -> str:
+    if not os.path.exists(GRAPH_SO):
+        build_graph_lib()
+    return GRAPH_SO
+
+
+def build_all(force: bool = False) -> None:
+    build_engine(force)
+    build_graph_lib(force)
+    build_oracle()

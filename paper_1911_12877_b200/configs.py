@@ -1,0 +1,106 @@
+"""The five BASELINE.json workloads as seeded synthetic graphs + plans.
+
+BASELINE.json names no public dataset; the graphs are generated from a seed
+with the shapes the configs state.  cfg3/cfg5 echo
+LiveJournal / Orkut sizes but are synthetic stand-ins.
+Generated CSRs are cached under $SMG_GRAPH_CACHE (default
+/tmp/symmine_graphs) as .npz; the cache is an optimisation only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .graph import Graph
+from .plan import Plan, motif_plans, named_plan
+
+CACHE = os.environ.get("SMG_GRAPH_CACHE", "/tmp/symmine_graphs")
+
+
+@dataclass(frozen=True)
+class GraphSpec:
+    kind: str      # "er" | "rmat" | "chung_lu"
+    params: tuple
+    seed: int
+
+    @property
+    def tag(self) -> str:
+        return f"{self.kind}_" + "_".join(str(p) for p in self.params) + f"_s{self.seed}"
+
+
+SPECS = {
+    # cfg1: ER n=65,536, m=1,048,576 distinct edges
+    "cfg1": GraphSpec("er", (65536, 1048576), 1),
+    # cfg2: RMAT scale 20, edge factor 16, (0.57,0.19,0.19,0.05), ids permuted
+    "cfg2": GraphSpec("rmat", (20, 16, 0.57, 0.19, 0.19), 2),
+    # cfg3: Chung-Lu n=4M, 43M edges, gamma 2.1, w_max 20,000
+    "cfg3": GraphSpec("chung_lu", (4000000, 43000000, 2.1, 20000.0), 3),
+    # cfg4: RMAT scale 22, edge factor 16
+    "cfg4": GraphSpec("rmat", (22, 16, 0.57, 0.19, 0.19), 4),
+    # cfg5: Chung-Lu n=3M, 117M edges, gamma 2.3, w_max 30,000
+    "cfg5": GraphSpec("chung_lu", (3000000, 117000000, 2.3, 30000.0), 5),
+}
+
+
+def config_patterns(cfg: str) -> list[tuple[str, Plan]]:
+    """(label, plan) pairs counted on each config."""
+    if cfg == "cfg1":
+        return [("triangle", named_plan("triangle"))]
+    if cfg == "cfg2":
+        return [("clique4", named_plan("clique", 4)), ("rectangle", named_plan("rectangle"))]
+    if cfg == "cfg3":
+        return [("clique5", named_plan("clique", 5)), ("house", named_plan("house"))]
+    if cfg == "cfg4":
+        return [(f"motif4:{r['name']}", r["plan"]) for r in motif_plans(4)]
+    if cfg == "cfg5":
+        return [("pentagon", named_plan("pentagon")),
+                ("tailed_diamond_a", named_plan("tailed_diamond_a")),
+                ("tailed_diamond_b", named_plan("tailed_diamond_b"))]
+    raise KeyError(cfg)
+
+
+def generate(spec: GraphSpec) -> Graph:
+    lib = N.graph_lib()
+    h = ctypes.c_void_p()
+    if spec.kind == "er":
+        n, m = spec.params
+        N.check_graph(lib.smg_gen_er(n, m, spec.seed, ctypes.byref(h)))
+    elif spec.kind == "rmat":
+        scale, ef, a, b, c = spec.params
+        N.check_graph(lib.smg_gen_rmat(scale, ef, a, b, c, spec.seed, ctypes.byref(h)))
+    elif spec.kind == "chung_lu":
+        n, m, gamma, wmax = spec.params
+        N.check_graph(lib.smg_gen_chung_lu(n, m, gamma, wmax, spec.seed, ctypes.byref(h)))
+    else:
+        raise N.InputError(f"unknown graph kind {spec.kind}")
+    return Graph._from_handle(h)
+
+
+def load(cfg_or_spec, cache: bool = True, verbose: bool = False) -> Graph:
+    spec = SPECS[cfg_or_spec] if isinstance(cfg_or_spec, str) else cfg_or_spec
+    path = os.path.join(CACHE, spec.tag + ".npz")
+    if cache and os.path.exists(path):
+        try:
+            z = np.load(path)
+            return Graph(z["offsets"], z["adjacency"], check=False)
+        except Exception:
+            pass
+    t0 = time.time()
+    g = generate(spec)
+    if verbose:
+        print(f"[configs] generated {spec.tag}: n={g.n} m={g.m} maxdeg={g.max_degree} "
+              f"in {time.time() - t0:.1f}s", flush=True)
+    if cache:
+        try:
+            os.makedirs(CACHE, exist_ok=True)
+            tmp = path + f".{os.getpid()}.tmp.npz"
+            np.savez(tmp, offsets=g.offsets, adjacency=g.adjacency)
+            os.replace(tmp, path)
+        except OSError:
+            pass
+    return g

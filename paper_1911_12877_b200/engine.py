@@ -1,0 +1,101 @@
+"""Python face of the C ABI: the reference's engine entry points on B200.
+
+    count(graph, plan, gpus=1)           ~ symmine.count(graph, plan, workers)
+                                           (python/module.cpp:162-167 -> count_instances,
+                                            engine.cpp:145-179)
+    count_pattern(graph, name, gpus=1)   ~ symmine.count_pattern (module.cpp:168-175)
+    motif_counts(graph, k, gpus=1)       ~ symmine.motif_counts (module.cpp:182-196,
+                                            engine.cpp:193-205)
+    count_range(graph, plan, lo, hi)     ~ Executor::count_range (engine.cpp:36-43)
+    count_shard(graph, plan, shard, n)   one rank's share of the level-1 units
+
+Every call runs on the GPU through libsymmine_gpu.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+from . import _native as N
+from .graph import Graph
+from .plan import Plan, motif_plans, named_plan
+
+
+@dataclass
+class CountResult:
+    """CountResult (engine.hpp:11-15) plus device counters."""
+
+    count: int
+    per_gpu: list = field(default_factory=list)
+    elements: int = 0   # E, intersected elements (meter=True only)
+    units: int = 0      # level-1 partial embeddings processed
+    wall_ms: float = 0.0
+    kernel_ms: float = 0.0
+
+
+def _result(r: N.SmgResult, ngpu: int) -> CountResult:
+    return CountResult(int(r.count), [int(r.per_gpu[i]) for i in range(ngpu)], int(r.elements),
+                       int(r.units), float(r.wall_ms), float(r.kernel_ms))
+
+
+def _plan(plan) -> Plan:
+    if isinstance(plan, Plan):
+        return plan
+    if isinstance(plan, (str, dict)):
+        return Plan.from_json(plan)
+    raise N.InputError("plan must be a Plan or plan JSON")
+
+
+def count_result(graph: Graph, plan, gpus: int = 1, meter: bool = False) -> CountResult:
+    """count_instances(g, plan, workers=gpus) on `gpus` B200s (one process)."""
+    p = _plan(plan)
+    gpus = max(1, int(gpus))  # workers == 0 -> 1 (engine.cpp:146)
+    lib = N.gpu_lib()
+    h = graph.device_handle(tuple(range(gpus)))
+    sp = p.to_smg()
+    r = N.SmgResult()
+    N.check_gpu(lib.smg_count(h, ctypes.byref(sp), gpus, N.SMG_METER if meter else 0, ctypes.byref(r)))
+    return _result(r, gpus)
+
+
+def count(graph: Graph, plan, gpus: int = 1) -> int:
+    return count_result(graph, plan, gpus).count
+
+
+def count_pattern(graph: Graph, name: str, k: int = 0, gpus: int = 1) -> int:
+    return count(graph, named_plan(name, k), gpus)
+
+
+def motif_counts(graph: Graph, k: int, gpus: int = 1) -> list[dict]:
+    out = []
+    for rec in motif_plans(k):
+        out.append({"bits": rec["bits"], "name": rec["name"], "key": rec["key"],
+                    "count": count(graph, rec["plan"], gpus)})
+    return out
+
+
+def count_range(graph: Graph, plan, lo: int, hi: int, device: int = 0, meter: bool = False) -> CountResult:
+    p = _plan(plan)
+    lib = N.gpu_lib()
+    h = graph.device_handle((device,))
+    sp = p.to_smg()
+    r = N.SmgResult()
+    N.check_gpu(lib.smg_count_range(h, ctypes.byref(sp), 0, lo, hi, N.SMG_METER if meter else 0,
+                                    ctypes.byref(r)))
+    return _result(r, 1)
+
+
+def count_shard(graph: Graph, plan, shard: int, num_shards: int, device: int = 0,
+                meter: bool = False) -> CountResult:
+    p = _plan(plan)
+    lib = N.gpu_lib()
+    h = graph.device_handle((device,))
+    sp = p.to_smg()
+    r = N.SmgResult()
+    N.check_gpu(lib.smg_count_shard(h, ctypes.byref(sp), 0, shard, num_shards,
+                                    N.SMG_METER if meter else 0, ctypes.byref(r)))
+    return _result(r, 1)
+
+
+def device_count() -> int:
+    return int(N.gpu_lib().smg_device_count())

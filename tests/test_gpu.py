@@ -1,0 +1,143 @@
+"""Parity of the CUDA engine (through the C ABI) with the reference.
+
+Golden fixtures come from the reference itself (tests/golden/make_golden.py);
+mid-size cases are checked against the C restatement (oracle/, pinned by
+tests/test_oracle.py); at BASELINE sizes the checks are the reference's own
+root-window counts plus size-independent invariants (shard partition,
+bounds on/off, orientation invariance, restrictions off = |Aut| x count).
+All counts must be bit-exact (uint64)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from common import er_graph
+from paper_1911_12877_b200 import (Graph, InputError, Plan, count, count_range, count_result,
+                                   count_shard, motif_counts, named_plan)
+from paper_1911_12877_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def corpus_graphs(golden):
+    return {k: Graph.from_edges(v["n"], v["edges"]) for k, v in golden["graphs"].items()}
+
+
+def _plan(golden, rec):
+    p = Plan.from_json(golden["plans"][rec["plan"]])
+    return p.with_options(rec["use_restrictions"], rec["use_bounds"]) if rec["use_restrictions"] \
+        else p.with_options(False, rec["use_bounds"])
+
+
+def test_golden_corpus_counts(golden, corpus_graphs):
+    bad = []
+    for rec in golden["counts"]:
+        c = count(corpus_graphs[rec["graph"]], _plan(golden, rec))
+        if c != rec["count"]:
+            bad.append((rec, c))
+    assert not bad, bad[:5]
+
+
+def test_golden_per_root_counts(golden, corpus_graphs):
+    for rec in golden["per_root"]:
+        g = corpus_graphs[rec["graph"]]
+        p = Plan.from_json(golden["plans"][rec["plan"]])
+        per = [count_range(g, p, v, v + 1).count for v in range(g.n)]
+        assert per == rec["counts"], (rec["graph"], rec["plan"])
+
+
+def test_elements_match_oracle(golden, corpus_graphs, port):
+    for gname in ("er_30_0.6_3030", "er_30_0.3_2030", "petersen", "K8", "empty4"):
+        g = corpus_graphs[gname]
+        for pname in ("triangle", "rectangle", "house", "pentagon", "clique:5", "motif4:101100",
+                      "star:5", "tailed_diamond_b", "clique:2"):
+            p = Plan.from_json(golden["plans"][pname])
+            r = count_result(g, p, meter=True)
+            c, e = port.count(g.offsets, g.adjacency, p.to_smg())
+            assert (r.count, r.elements) == (c, e), (gname, pname)
+            unbounded = count_result(g, p.with_options(True, False), meter=True)
+            assert (unbounded.count, unbounded.elements) == (c, e)
+
+
+def test_shards_partition_units(golden, corpus_graphs):
+    g = corpus_graphs["er_30_0.6_3030"]
+    for pname in ("triangle", "house", "clique:4", "pentagon"):
+        p = Plan.from_json(golden["plans"][pname])
+        full = count_result(g, p)
+        for s in (2, 3, 8):
+            parts = [count_shard(g, p, i, s) for i in range(s)]
+            assert sum(r.count for r in parts) == full.count
+            assert sum(r.units for r in parts) == full.units
+
+
+def test_invalid_plan_raises_input_error():
+    g = Graph.from_edges(3, [(0, 1), (1, 2), (0, 2)])
+    sp = named_plan("triangle")
+    bad = Plan(sp.n, sp.edges, sp.schedule, [lv for lv in sp.levels])
+    bad.levels = list(sp.levels)
+    from paper_1911_12877_b200.plan import PlanLevel
+    bad.levels[2] = PlanLevel([0, 1], [], 2)  # parent not earlier
+    with pytest.raises(InputError):
+        count(g, bad)
+
+
+def test_motif_counts_api():
+    g = Graph.from_edges(*er_graph(30, 0.3, 4030))
+    from oracle.ref import Port
+    port = Port()
+    res = motif_counts(g, 4)
+    assert len(res) == 6
+    for r, rec in zip(res, __import__("paper_1911_12877_b200").motif_plans(4)):
+        assert r["count"] == port.count(g.offsets, g.adjacency, rec["plan"].to_smg())[0]
+
+
+MID_PLANS = ["triangle", "rectangle", "house", "pentagon", "clique:4", "clique:5",
+             "tailed_diamond_a", "tailed_diamond_b", "path:4", "star:4", "hourglass",
+             "clique_minus:5"]
+
+
+@pytest.mark.parametrize("spec", [configs.GraphSpec("rmat", (12, 8, 0.57, 0.19, 0.19), 11),
+                                  configs.GraphSpec("chung_lu", (6000, 60000, 2.1, 600.0), 12),
+                                  configs.GraphSpec("er", (3000, 30000), 13)],
+                         ids=lambda s: s.tag)
+def test_mid_size_vs_oracle(spec, port):
+    g = configs.load(spec)
+    for name in MID_PLANS:
+        p = named_plan(name)
+        r = count_result(g, p, meter=True)
+        c, e = port.count(g.offsets, g.adjacency, p.to_smg(), threads=8)
+        assert (r.count, r.elements) == (c, e), name
+    for rec in __import__("paper_1911_12877_b200").motif_plans(4):
+        c, _ = port.count(g.offsets, g.adjacency, rec["plan"].to_smg(), threads=8)
+        assert count(g, rec["plan"]) == c, rec["name"]
+
+
+def test_cfg1_triangle_full_count(golden_configs, port):
+    g = configs.load("cfg1")
+    r = count_result(g, named_plan("triangle"), meter=True)
+    assert r.count == golden_configs["cfg1"]["full"]["triangle"]["count"]
+    c, e = port.count(g.offsets, g.adjacency, named_plan("triangle").to_smg(), threads=8)
+    assert (r.count, r.elements) == (c, e)
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    return configs.load("cfg2")
+
+
+def test_cfg2_reference_root_windows(golden_configs, cfg2):
+    for label, plan in configs.config_patterns("cfg2"):
+        for w in golden_configs["cfg2"]["root_windows"][label]:
+            assert count_range(cfg2, plan, w["lo"], w["hi"]).count == w["count"], (label, w)
+
+
+def test_cfg2_full_size_invariants(cfg2):
+    p = named_plan("clique", 4)
+    full = count_result(cfg2, p)
+    assert count(cfg2, p.with_options(True, False)) == full.count          # bounds on/off
+    assert sum(count_shard(cfg2, p, i, 4).count for i in range(4)) == full.count
+    assert count(cfg2.orient(), p) == full.count                             # orientation
+    # restrictions off counts every automorphic mapping: |Aut(clique4)| = 24
+    tri = named_plan("triangle")
+    assert count(cfg2, tri.with_options(False, True)) == 6 * count(cfg2, tri)
