@@ -79,6 +79,7 @@ def build_oracle(reference: bool | None = None) -> None:
         reference = os.path.isdir(REFERENCE)
     if reference:
         subprocess.run(["make", "-s", "-j8", "-C", ORACLE_DIR, "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", ORACLE_DIR, "adapter"], check=True)
 
 
 def ensure_engine() -> str:

@@ -68,7 +68,15 @@ struct Program {
   int8_t node_begin[kMaxLevels];  // nodes built at loop k: [node_begin[k], node_end[k])
   int8_t node_end[kMaxLevels];
   int8_t unit_bound;              // level 1 requires v1 < v0
-  int8_t pad[7];
+  // Leaf batching: when the leaf is `src (op) N(v_{n-2})`, the counts of all
+  // siblings v_{n-2} in C_{n-2} are one edge count between two sets,
+  //   sum_{x in C_{n-2}} |B & N(x)|,  B = the leaf's source set,
+  // evaluated at loop n-3 (engine.cu, leaf_batch).
+  int8_t batch;                   // 1 if the leaf can be batched
+  int8_t batch_diff;              // leaf op is -N[x] (else & N(x))
+  int8_t batch_yltx;              // leaf bound is x itself (y < x)
+  int8_t batch_fixed_bound;       // leaf bound level < n-2 (fixed over siblings), -1 none
+  int8_t pad[3];
   Node leaf;                      // C_{depth-1}, counted not stored (depth >= 3)
   Node nodes[kMaxNodes];
 };
@@ -192,6 +200,13 @@ inline std::string compile_program(const smg_plan& p, Program* out) {
     if (pr.cand[i] >= 0) pr.cand[i] = static_cast<int8_t>(remap[pr.cand[i]]);
   pr.nnodes = nt;
   pr.nslots = slots;
+  pr.batch_fixed_bound = -1;
+  if (n >= 4 && pr.leaf.src >= 0 && pr.leaf.nops == 1 && pr.leaf.ops[0].level == n - 2) {
+    pr.batch = 1;
+    pr.batch_diff = pr.leaf.ops[0].mode == kOpDiff ? 1 : 0;
+    pr.batch_yltx = pr.leaf.bound == n - 2 ? 1 : 0;
+    if (pr.leaf.bound >= 0 && pr.leaf.bound < n - 2) pr.batch_fixed_bound = pr.leaf.bound;
+  }
   *out = pr;
   return "";
 }

@@ -15,6 +15,18 @@ from . import _native as N
 from .engine import CountResult, count_shard
 
 
+SHARD_CHUNK = 32  # kChunk in csrc/engine.cu: edge slots per work-queue grab
+
+
+def shard_slots(num_slots: int, shard: int, num_shards: int):
+    """The edge slots shard `shard` of `num_shards` owns: global chunk g (slots
+    [32g, 32g+32)) belongs to shard g % num_shards -- the mapping count_kernel
+    applies to its dynamic queue (gchunk = chunk * num_shards + shard)."""
+    import numpy as np
+    e = np.arange(num_slots, dtype=np.uint64)
+    return e[(e // SHARD_CHUNK) % num_shards == shard]
+
+
 def split_u64(values):
     lo = [int(v) & 0xFFFFFFFF for v in values]
     hi = [int(v) >> 32 for v in values]

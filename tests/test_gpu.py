@@ -71,6 +71,23 @@ def test_shards_partition_units(golden, corpus_graphs):
             assert sum(r.units for r in parts) == full.units
 
 
+def test_shard_units_follow_host_mapping(golden, corpus_graphs, port):
+    """The device's chunk->shard map is the one distributed.shard_slots states
+    (the gloo test relies on it)."""
+    from paper_1911_12877_b200.distributed import shard_slots
+    g = corpus_graphs["er_30_0.6_3030"]
+    src = np.repeat(np.arange(g.n), np.diff(g.offsets).astype(np.int64))
+    p = Plan.from_json(golden["plans"]["house"])
+    for s in (2, 3):
+        for i in range(s):
+            slots = shard_slots(g.adjacency.size, i, s).astype(np.int64)
+            valid = int((g.adjacency[slots] < src[slots]).sum())
+            r = count_shard(g, p, i, s)
+            assert r.units == valid
+            c, _ = port.count_edges(g.offsets, g.adjacency, p.to_smg(), slots)
+            assert r.count == c
+
+
 def test_invalid_plan_raises_input_error():
     g = Graph.from_edges(3, [(0, 1), (1, 2), (0, 2)])
     sp = named_plan("triangle")
@@ -141,3 +158,17 @@ def test_cfg2_full_size_invariants(cfg2):
     # restrictions off counts every automorphic mapping: |Aut(clique4)| = 24
     tri = named_plan("triangle")
     assert count(cfg2, tri.with_options(False, True)) == 6 * count(cfg2, tri)
+
+
+def test_cpp_adapter_drop_in():
+    """include/symmine_gpu.hpp used from C++ with the reference's own front end
+    and engine (binary built in the dev container by `make -C oracle adapter`)."""
+    import os
+    import subprocess
+    from common import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "adapter_drop_in")
+    if not os.path.exists(exe):
+        pytest.skip("adapter binary not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.strip().endswith("OK")

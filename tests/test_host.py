@@ -108,7 +108,31 @@ def describe(plan: Plan) -> dict:
     return json.loads(buf.value.decode())
 
 
-def run_program(prog, off, adj):
+def leaf_batch_model(prog, vals, sets, nb):
+    """engine.cu leaf_batch: sum over siblings x in C_{n-2} of the leaf count,
+    as an edge count between A = C_{n-2} and B = the leaf source set."""
+    depth = prog["depth"]
+    A = sets[prog["cand"][depth - 2]]
+    B = sets[prog["leaf"]["src"]]
+    if prog["batch_fixed_bound"] >= 0:
+        B = [y for y in B if y < vals[prog["batch_fixed_bound"]]]
+    yltx = prog["batch_yltx"]
+    Bs = set(B)
+    # core, from whichever side (symmetric adjacency): check both agree
+    core_a = sum(1 for x in A for y in nb[x] if y in Bs and (not yltx or y < x))
+    As = set(A)
+    core_b = sum(1 for y in B for x in nb[y] if x in As and (not yltx or y < x))
+    assert core_a == core_b
+    if not prog["batch_diff"]:
+        return core_a
+    if yltx:
+        t1, t2 = sum(sum(1 for y in B if y < x) for x in A), 0
+    else:
+        t1, t2 = len(A) * len(B), sum(1 for x in A if x in Bs)
+    return t1 - t2 - core_a
+
+
+def run_program(prog, off, adj, batch=False):
     """Execute the program exactly as count_kernel does (engine.cu)."""
     n = len(off) - 1
     nb = [set(adj[off[v]:off[v + 1]].tolist()) for v in range(n)]
@@ -129,6 +153,8 @@ def run_program(prog, off, adj):
         for t in range(prog["node_begin"][k], prog["node_end"][k]):
             sets[t] = node_set(prog["nodes"][t], vals, sets)
 
+    use_batch = batch and prog["batch"]
+
     def dfs(level, vals, sets):
         nonlocal total
         for x in sets[prog["cand"][level]]:
@@ -136,6 +162,8 @@ def run_program(prog, off, adj):
             build(level, vals, sets)
             if level == depth - 2:
                 total += len(node_set(prog["leaf"], vals, sets))
+            elif use_batch and level == depth - 3:
+                total += leaf_batch_model(prog, vals, sets, nb)
             else:
                 dfs(level + 1, vals, sets)
 
@@ -152,6 +180,8 @@ def run_program(prog, off, adj):
             build(1, vals, sets)
             if depth == 3:
                 total += len(node_set(prog["leaf"], vals, sets))
+            elif use_batch and depth == 4:
+                total += leaf_batch_model(prog, vals, sets, nb)
             else:
                 dfs(2, vals, sets)
     return total
@@ -185,5 +215,16 @@ def test_program_interpreter_matches_reference_golden(golden, port):
         if g["n"] > 15 and not rec["use_restrictions"] and progs[key]["depth"] >= 5:
             continue
         assert run_program(progs[key], off, adj) == rec["count"], rec
+        if g["n"] <= 15:
+            assert run_program(progs[key], off, adj, batch=True) == rec["count"], rec
         checked += 1
     assert checked > 1500
+
+
+def test_batchable_plans():
+    for name, k in (("clique", 4), ("rectangle", 0), ("house", 0), ("pentagon", 0), ("clique", 5)):
+        assert describe(named_plan(name, k))["batch"] == 1, name
+    for rec in __import__("paper_1911_12877_b200").motif_plans(4):
+        assert describe(rec["plan"])["batch"] == 1, rec["name"]
+    # leaf with a single intersect source (the last level): not batched
+    assert describe(named_plan("path", 4))["batch"] == 0
