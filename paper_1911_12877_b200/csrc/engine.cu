@@ -41,14 +41,14 @@ constexpr int kHashLog2 = 11;  // per-warp shared-memory hash: 2048 slots (8 KB)
 constexpr uint32_t kHashSlots = 1u << kHashLog2;
 constexpr uint32_t kEmptySlot = 0xffffffffu;  // never a vertex id (ids < n < 2^32)
 constexpr size_t kDynSmem = sizeof(uint32_t) * kHashSlots * kWarpsPerBlock;
-// CTA tier (heavy_kernel): 16 warps share one 32K-slot (128 KB) table.
-constexpr int kHeavyWarps = 16;
+// CTA tier (heavy_kernel): 16 warps share one 16K-slot (64 KB) table.
+constexpr int kHeavyWarps = 8;
 constexpr int kHeavyThreads = kHeavyWarps * 32;
-constexpr uint32_t kHeavySlots = 1u << 15;
+constexpr uint32_t kHeavySlots = 1u << 13;  // 32 KB: four CTAs per SM overlap their phases
 constexpr uint32_t kHeavyChunk = kHeavySlots / 2;  // probe-set elements per table fill
 constexpr size_t kHeavySmem = sizeof(uint32_t) * kHeavySlots;
 constexpr uint64_t kHeavyMinStream = 4096;  // defer only batches with real streaming work
-constexpr uint64_t kHeavyQueueCap = 1ull << 22;
+constexpr uint64_t kHeavyQueueCap = 1ull << 24;
 
 // ---------------------------------------------------------------- device ---
 
@@ -62,13 +62,13 @@ struct Counters {
   unsigned int overflow;
   unsigned int pad;
   // SMG_TRACE=1: per-phase cycle and event counters (see kTr* below)
-  unsigned long long trace[16];  // >= kTrCount
+  unsigned long long trace[32];  // >= kTrCount
 };
 
 enum {
   kTrUnits = 0, kTrBuildCycles, kTrBatchCycles, kTrBatches, kTrBatchesHashed, kTrStreamElems,
   kTrSearchLists, kTrProbeSetSum, kTrStreamSetSum, kTrLeafCycles, kTrLeaves, kTrBigPCycles,
-  kTrDeferred, kTrHeavyItems, kTrHeavyCycles, kTrCount
+  kTrDeferred, kTrHeavyItems, kTrHeavyCycles, kTrLongLists, kTrHeavyBuild, kTrHeavyStream, kTrCount
 };
 
 struct KernelArgs {
@@ -158,34 +158,207 @@ __device__ __forceinline__ void nbrs(const Ctx& c, uint32_t v, const uint32_t*& 
   len = static_cast<uint32_t>(e - b);
 }
 
+// ------------------------------------------------------------ set ops ---
+// Every set operation streams one sorted list with coalesced, unrolled warp
+// loads and tests membership in the other operand through a ProbeSet: a
+// shared-memory hash table when the operand is small enough (build cost
+// |operand| inserts, probe ~1-2 LDS), else a branchless binary search.  The
+// side to stream and the probe structure are chosen per pair from the two
+// lengths: tiny-vs-large pairs (hub lists) binary-search the few elements;
+// comparable or moderately skewed pairs hash the smaller side and stream the
+// larger.  Bounds arrive as prefix truncations (set_ops.hpp:20-25).
+
+struct ProbeSet {
+  const uint32_t* arr;  // sorted (scratch or CSR slice)
+  uint32_t n;
+  uint32_t lo, hi;      // arr[0], arr[n-1]
+  uint32_t* hash;       // shared-memory table, valid when bits > 0
+  int bits;
+};
+
+// The table is bucketised: a key hashes to a bucket of 4 consecutive slots
+// (one 16-byte LDS.128), buckets fill in slot order and overflow linearly
+// into the next bucket only when full, so a lookup stops at the first bucket
+// whose last slot is empty.  At load <= 1/2 nearly every lookup (hit or
+// miss) is one LDS.128, and the warp no longer waits for the longest of 32
+// linear-probe chains.
+__device__ __forceinline__ uint32_t hbucket(uint32_t x, int bbits) {
+  return (x * 0x9E3779B1u) >> (32 - bbits);
+}
+
+__device__ __forceinline__ bool probe(const ProbeSet& P, uint32_t y) {
+  if (P.bits) {
+    const int bbits = P.bits - 2;
+    const uint32_t mask = (1u << bbits) - 1u;
+    const uint4* tb = reinterpret_cast<const uint4*>(P.hash);
+    uint32_t h = hbucket(y, bbits);
+    for (;;) {
+      const uint4 q = tb[h];
+      if (q.x == y || q.y == y || q.z == y || q.w == y) return true;
+      if (q.w == kEmptySlot) return false;
+      h = (h + 1) & mask;
+    }
+  }
+  return contains_rw(P.arr, P.n, y);
+}
+
+__device__ __forceinline__ int table_bits(uint32_t n) {
+  int bits = 6;
+  while ((1u << bits) < 2 * n) ++bits;
+  return bits;
+}
+
+// Cooperative table fill by threads [tid, tid+nthreads); the caller syncs
+// between the two phases and after.  Requires 2 * P.n <= table capacity.
+__device__ __forceinline__ void fill_table(uint32_t* table, const ProbeSet& P, int tid,
+                                           int nthreads) {
+  const uint32_t nb = 1u << (P.bits - 2);
+  uint4* tb = reinterpret_cast<uint4*>(table);
+  for (uint32_t i = tid; i < nb; i += nthreads) tb[i] = make_uint4(kEmptySlot, kEmptySlot, kEmptySlot, kEmptySlot);
+}
+
+__device__ __forceinline__ void insert_table(uint32_t* table, const ProbeSet& P, int tid,
+                                             int nthreads) {
+  const int bbits = P.bits - 2;
+  const uint32_t mask = (1u << bbits) - 1u;
+  for (uint32_t i = tid; i < P.n; i += nthreads) {
+    const uint32_t key = P.arr[i];
+    uint32_t h = hbucket(key, bbits);
+    for (;;) {
+      uint32_t* bk = table + 4 * h;
+      if (atomicCAS(bk, kEmptySlot, key) == kEmptySlot || atomicCAS(bk + 1, kEmptySlot, key) == kEmptySlot ||
+          atomicCAS(bk + 2, kEmptySlot, key) == kEmptySlot || atomicCAS(bk + 3, kEmptySlot, key) == kEmptySlot)
+        break;
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+// A ProbeSet over arr[0..n) (n > 0): hashed into the warp's table if it fits
+// and `hash` is requested, else binary search.
+__device__ __forceinline__ ProbeSet make_probe(const Ctx& c, const uint32_t* arr, uint32_t n,
+                                               bool hash) {
+  ProbeSet p;
+  p.arr = arr;
+  p.n = n;
+  p.lo = arr[0];
+  p.hi = arr[n - 1];
+  p.hash = c.hash;
+  p.bits = 0;
+  if (hash && 2 * n <= kHashSlots) {
+    p.bits = table_bits(n);
+    __syncwarp();
+    fill_table(c.hash, p, c.lane, 32);
+    __syncwarp();
+    insert_table(c.hash, p, c.lane, 32);
+    __syncwarp();
+  }
+  return p;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += t;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+  return v;  // every lane holds the sum
+}
+
+constexpr int kUnroll = 4;  // independent loads in flight per lane
+
+__device__ __forceinline__ int ilog2p1(uint32_t x) { return 32 - __clz(x | 1u); }
+
+// Hash the small side and stream the large one, or binary-search the small
+// side into the large one?  Per-warp cycle model: a binary-search round costs
+// ~log2(large) dependent loads, a stream iteration ~one load latency per
+// 32*kUnroll elements.
+__device__ __forceinline__ bool prefer_stream(uint32_t small, uint32_t large) {
+  if (small * 2 > kHashSlots) return false;
+  const uint64_t bs = static_cast<uint64_t>((small + 31) / 32) * ilog2p1(large);
+  const uint64_t st = (large + 32 * kUnroll - 1) / (32 * kUnroll) + (small + 31) / 32;
+  return st < bs;
+}
+
+// Stream X[0..nX), keep x iff (x in Pr) == keep_found and x != exclude.
+// COUNT: return the number kept; else also write them, in order, to out.
+template <bool COUNT>
+__device__ uint32_t filter_list(const Ctx& c, const uint32_t* X, uint32_t nX, const ProbeSet& Pr,
+                                bool keep_found, uint32_t exclude, uint32_t* out) {
+  const unsigned lt_mask = (1u << c.lane) - 1u;
+  uint32_t written = 0;
+  for (uint32_t base = 0; base < nX; base += 32 * kUnroll) {
+    uint32_t x[kUnroll];
+    bool ok[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32 + c.lane;
+      ok[u] = i < nX;
+      x[u] = ok[u] ? X[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      bool keep = ok[u] && x[u] != exclude;
+      if (keep) keep = probe(Pr, x[u]) == keep_found;
+      const unsigned m = __ballot_sync(kFull, keep);
+      if (!COUNT && keep) out[written + __popc(m & lt_mask)] = x[u];
+      written += __popc(m);
+    }
+  }
+  return written;
+}
+
 // Apply a node's ops to the input set `in` (sorted, already bounded).
 // COUNT: return |result| only; else write the sorted result to `out`.
 template <bool COUNT>
 __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, uint32_t inlen,
-                              bool in_is_scratch, uint32_t* out) {
+                              uint32_t* out) {
   const WarpState& s = *c.s;
-  const unsigned lt_mask = (1u << c.lane) - 1u;
-  // Single intersection: iterate the shorter side, probe the longer.
-  if (nd.nops == 1 && nd.ops[0].mode == kOpIsect) {
-    const uint32_t* b;
-    uint32_t blen;
-    nbrs(c, s.vals[nd.ops[0].level], b, blen);
-    if (nd.bound >= 0) blen = lower_bound_dev(b, blen, s.vals[nd.bound]);
-    if (blen < inlen) {
-      uint32_t written = 0;
-      for (uint32_t base = 0; base < blen; base += 32) {
-        const uint32_t i = base + c.lane;
-        bool keep = i < blen;
-        const uint32_t x = keep ? __ldg(b + i) : 0u;
-        if (keep) keep = in_is_scratch ? contains_rw(in, inlen, x) : contains_dev(in, inlen, x);
-        const unsigned m = __ballot_sync(kFull, keep);
-        if (!COUNT && keep) out[written + __popc(m & lt_mask)] = x;
-        written += __popc(m);
+  if (inlen == 0) return 0;
+  if (nd.nops == 1) {
+    const uint32_t v = s.vals[nd.ops[0].level];
+    const uint32_t* L;
+    uint32_t nL;
+    nbrs(c, v, L, nL);
+    if (nd.ops[0].mode == kOpIsect) {
+      if (nd.bound >= 0) nL = lower_bound_dev(L, nL, s.vals[nd.bound]);
+      if (nL == 0) return 0;
+      // result = in & L; iterate either side (both sorted -> sorted output)
+      const bool in_small = inlen <= nL;
+      const uint32_t* Sm = in_small ? in : L;
+      const uint32_t nSm = in_small ? inlen : nL;
+      const uint32_t* Lg = in_small ? L : in;
+      const uint32_t nLg = in_small ? nL : inlen;
+      if (prefer_stream(nSm, nLg)) {
+        const ProbeSet pr = make_probe(c, Sm, nSm, true);
+        return filter_list<COUNT>(c, Lg, nLg, pr, true, kEmptySlot, out);
       }
-      return written;
+      const ProbeSet pr = make_probe(c, Lg, nLg, false);
+      return filter_list<COUNT>(c, Sm, nSm, pr, true, kEmptySlot, out);
     }
+    // result = in - N[v]: stream `in`; only N(v) within [in.lo, in.hi] matters
+    const uint32_t lo = in[0], hi = in[inlen - 1];
+    const uint32_t a = lower_bound_dev(L, nL, lo);
+    const uint32_t b = lower_bound_dev(L, nL, hi + 1u);  // independent of a: overlaps
+    if (b == a) {  // nothing to subtract but v itself
+      ProbeSet none;
+      none.arr = L;
+      none.n = 0;
+      none.bits = 0;
+      return filter_list<COUNT>(c, in, inlen, none, false, v, out);
+    }
+    const bool hash = 2 * (b - a) <= kHashSlots && (b - a) <= 8u * inlen;
+    const ProbeSet pr = make_probe(c, L + a, b - a, hash);
+    return filter_list<COUNT>(c, in, inlen, pr, false, v, out);
   }
-  // Generic: iterate the input, probe every op list.
+  // Several ops (a start node with earlier differences): binary-search all.
+  const unsigned lt_mask = (1u << c.lane) - 1u;
   const uint32_t* opp[kMaxOps];
   uint32_t opl[kMaxOps];
   uint32_t opv[kMaxOps];
@@ -197,7 +370,7 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
   for (uint32_t base = 0; base < inlen; base += 32) {
     const uint32_t i = base + c.lane;
     bool keep = i < inlen;
-    const uint32_t x = keep ? (in_is_scratch ? in[i] : __ldg(in + i)) : 0u;
+    const uint32_t x = keep ? in[i] : 0u;
     for (int o = 0; o < nd.nops; ++o) {
       if (keep) {
         const bool f = contains_dev(opp[o], opl[o], x);
@@ -213,41 +386,32 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
 
 // Resolve a node's input set (source node or raw list), bounded.
 __device__ __forceinline__ void node_input(const Ctx& c, const Node& nd, const uint32_t*& in,
-                                           uint32_t& inlen, bool& in_scratch) {
+                                           uint32_t& inlen) {
   const WarpState& s = *c.s;
   if (nd.src >= 0) {
     in = s.ptr[nd.src];
     inlen = s.len[nd.src];
-    in_scratch = true;  // may also be a raw CSR slice; plain loads are fine for both
   } else {
     nbrs(c, s.vals[nd.list], in, inlen);
-    in_scratch = false;
   }
-  if (nd.bound >= 0) {
-    const uint32_t b = s.vals[nd.bound];
-    inlen = in_scratch ? lower_bound_rw(in, inlen, b) : lower_bound_dev(in, inlen, b);
-  }
+  if (nd.bound >= 0) inlen = lower_bound_rw(in, inlen, s.vals[nd.bound]);
 }
 
 __device__ void build_node(const Ctx& c, const Program& P, int t) {
   const Node& nd = P.nodes[t];
   const uint32_t* in;
   uint32_t inlen;
-  bool in_scratch;
-  node_input(c, nd, in, inlen, in_scratch);
-  if (nd.raw) {
-    if (c.lane == 0) {
-      c.s->ptr[t] = in;
-      c.s->len[t] = inlen;
-    }
-    __syncwarp();
-    return;
+  node_input(c, nd, in, inlen);
+  uint32_t len = inlen;
+  const uint32_t* ptr = in;
+  if (!nd.raw) {
+    uint32_t* out = c.scratch + static_cast<uint64_t>(nd.slot) * c.cap;
+    len = apply_ops<false>(c, nd, in, inlen, out);
+    ptr = out;
   }
-  uint32_t* out = c.scratch + static_cast<uint64_t>(nd.slot) * c.cap;
-  const uint32_t len = apply_ops<false>(c, nd, in, inlen, in_scratch, out);
   __syncwarp();
   if (c.lane == 0) {
-    c.s->ptr[t] = out;
+    c.s->ptr[t] = ptr;
     c.s->len[t] = len;
   }
   __syncwarp();
@@ -256,10 +420,9 @@ __device__ void build_node(const Ctx& c, const Program& P, int t) {
 __device__ __forceinline__ uint32_t leaf_count(const Ctx& c, const Program& P) {
   const uint32_t* in;
   uint32_t inlen;
-  bool in_scratch;
-  node_input(c, P.leaf, in, inlen, in_scratch);
+  node_input(c, P.leaf, in, inlen);
   if (P.leaf.raw) return inlen;
-  return apply_ops<true>(c, P.leaf, in, inlen, in_scratch, nullptr);
+  return apply_ops<true>(c, P.leaf, in, inlen, nullptr);
 }
 
 // E contribution of building level i from the current prefix v_0..v_{i-1}:
@@ -274,6 +437,31 @@ __device__ __forceinline__ uint64_t meter_level(const Ctx& c, const Program& P, 
     term = (par >= 0) ? lower_bound_dev(p, len, c.s->vals[par]) : len;
   }
   return __reduce_add_sync(kFull, term);
+}
+
+// E of all leaf builds of a batch: for every sibling x in C_{n-2}, level n-1 is
+// built from v_0..v_{n-3}, x with bound beta (v_p, x itself, or none).
+__device__ uint64_t meter_batch(const Ctx& c, const Program& P) {
+  const WarpState& s = *c.s;
+  const int n = P.depth;
+  const int an = P.cand[n - 2];
+  const uint32_t* A = s.ptr[an];
+  const uint32_t nA = s.len[an];
+  const int par = P.parent[n - 1];
+  uint64_t acc = 0;
+  for (uint32_t i = c.lane; i < nA; i += 32) {
+    const uint32_t x = A[i];
+    const bool unbounded = par < 0;
+    const uint32_t beta = par < 0 ? 0u : (par == n - 2 ? x : s.vals[par]);
+    for (int j = 0; j <= n - 2; ++j) {
+      const uint32_t v = j == n - 2 ? x : s.vals[j];
+      const uint32_t* p;
+      uint32_t len;
+      nbrs(c, v, p, len);
+      acc += unbounded ? len : lower_bound_dev(p, len, beta);
+    }
+  }
+  return warp_sum64(acc);
 }
 
 __device__ __forceinline__ void checked_acc(uint64_t& acc, uint64_t add, bool& ovf) {
@@ -296,78 +484,19 @@ __device__ __forceinline__ void checked_acc(uint64_t& acc, uint64_t add, bool& o
 // Two tiers: a batch whose probe set fits the per-warp table (kHashSlots) runs
 // in the warp that found it; a bigger one with real streaming work is queued
 // (its prefix v_0..v_{n-3}) for heavy_kernel, where a whole CTA shares a
-// 128 KB table and streams the lists with all its warps.
+// 64 KB table and streams the lists with all its warps.
 
-struct ProbeSet {
-  const uint32_t* arr;  // sorted (scratch or CSR slice)
-  uint32_t n;
-  uint32_t lo, hi;      // arr[0], arr[n-1]
-  uint32_t* hash;       // shared-memory table, valid when bits > 0
-  int bits;
-};
-
-__device__ __forceinline__ uint32_t hslot(uint32_t x, int bits) {
-  return (x * 0x9E3779B1u) >> (32 - bits);
-}
-
-__device__ __forceinline__ bool probe(const ProbeSet& P, uint32_t y) {
-  if (P.bits) {
-    const uint32_t mask = (1u << P.bits) - 1u;
-    uint32_t h = hslot(y, P.bits);
-    for (;;) {
-      const uint32_t k = P.hash[h];
-      if (k == y) return true;
-      if (k == kEmptySlot) return false;
-      h = (h + 1) & mask;
-    }
-  }
-  return contains_rw(P.arr, P.n, y);
-}
-
-__device__ __forceinline__ int table_bits(uint32_t n) {
-  int bits = 6;
-  while ((1u << bits) < 2 * n) ++bits;
-  return bits;
-}
-
-// Fill `table` with P (threads [tid, tid+nthreads) cooperate; caller syncs
-// before and after).  Requires P.n > 0 and 2 * P.n <= table capacity.
-__device__ __forceinline__ void fill_table(uint32_t* table, const ProbeSet& P, int tid,
-                                           int nthreads) {
-  const uint32_t slots = 1u << P.bits;
-  for (uint32_t i = tid; i < slots; i += nthreads) table[i] = kEmptySlot;
-}
-
-__device__ __forceinline__ void insert_table(uint32_t* table, const ProbeSet& P, int tid,
-                                             int nthreads) {
-  const uint32_t mask = (1u << P.bits) - 1u;
-  for (uint32_t i = tid; i < P.n; i += nthreads) {
-    const uint32_t key = P.arr[i];
-    uint32_t h = hslot(key, P.bits);
-    while (atomicCAS(&table[h], kEmptySlot, key) != kEmptySlot) h = (h + 1) & mask;
-  }
-}
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t t = __shfl_up_sync(kFull, v, d);
-    if (lane >= d) v += t;
-  }
-  return v;
-}
-
-__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
-  return v;  // every lane holds the sum
-}
-
-constexpr int kStreamUnroll = 4;  // independent loads in flight per lane
+constexpr uint32_t kLongList = 64;  // lists this long are streamed by the whole warp
 
 // sum_{s in S} |{p in P : p in N(s)}| with rel: 0 none, 1 p < s, 2 p > s, over
 // the groups of 32 elements of S starting at g_first with stride g_stride.
-// Returns this warp's partial (all lanes hold it).
+// Each lane resolves one s and the value window [lo, hi) of P (and the rel
+// bound).  Long lists are then streamed one at a time by the whole warp
+// (coalesced, kUnroll loads in flight per lane, early exit at hi -- sorted
+// lists need no upper-bound search, and the lower one only when the list
+// starts below lo); short lists are flattened across the lanes; skewed pairs
+// (|P| log |N(s)| << |N(s)|) binary-search P into N(s).  Returns this warp's
+// partial (all lanes hold it).
 template <bool TRACE>
 __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, const ProbeSet& P,
                                  int rel, uint32_t g_first, uint32_t g_stride, uint64_t* tr) {
@@ -376,7 +505,7 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
     const uint32_t i = g0 + c.lane;
     uint32_t start = 0, len = 0, lo_val = P.lo, hi_val = P.hi + 1u;
     const uint32_t* base = c.adj;
-    bool search = false;
+    bool is_long = false, search = false;
     if (i < nS) {
       const uint32_t s = S[i];
       if (rel == 1) hi_val = min(hi_val, s);
@@ -385,50 +514,73 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
       base = c.adj + b;
       const uint32_t deg = static_cast<uint32_t>(e - b);
       if (lo_val < hi_val && deg) {
-        if (deg > 32) {
-          start = lower_bound_dev(base, deg, lo_val);
-          len = lower_bound_dev(base + start, deg - start, hi_val);
-        } else {
-          len = deg;  // short list: range-filter per element instead
+        const uint32_t first = __ldg(base), last = __ldg(base + deg - 1);
+        if (last >= lo_val && first < hi_val) {
+          len = deg;
+          if (deg >= kLongList) {
+            is_long = true;
+            if (first < lo_val) start = lower_bound_dev(base, deg, lo_val);
+            len = deg - start;
+            search = static_cast<uint64_t>(P.n) * ilog2p1(len) * 2u < len;
+            is_long = !search;
+          }
         }
       }
-      search = len > 64 && static_cast<uint64_t>(P.n) * (33u - __clz(len)) * 2u < len;
     }
-    const uint32_t slen = search ? 0u : len;
+    uint32_t hits = 0;
+    // 1) long lists: one at a time, whole warp, early exit at hi
+    unsigned lm = __ballot_sync(kFull, is_long);
+    if (TRACE) {
+      tr[kTrSearchLists] += __popc(__ballot_sync(kFull, search));
+      tr[kTrLongLists] += __popc(lm);
+    }
+    while (lm) {
+      const int j = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const uint32_t* jp = reinterpret_cast<const uint32_t*>(
+                               __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j)) +
+                           __shfl_sync(kFull, start, j);
+      const uint32_t jl = __shfl_sync(kFull, len, j);
+      const uint32_t jhi = __shfl_sync(kFull, hi_val, j);
+      for (uint32_t t0 = 0; t0 < jl; t0 += 32 * kUnroll) {
+        uint32_t y[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint32_t idx = t0 + u * 32 + c.lane;
+          y[u] = idx < jl ? __ldg(jp + idx) : kEmptySlot;
+        }
+        if (TRACE && c.lane == 0) tr[kTrStreamElems] += min(32u * kUnroll, jl - t0);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (y[u] < jhi && probe(P, y[u])) ++hits;
+        if (__any_sync(kFull, y[kUnroll - 1] >= jhi)) break;  // sorted: the rest is >= hi
+      }
+    }
+    // 2) short lists: flattened over the lanes, range-filtered per element
+    const uint32_t slen = is_long || search ? 0u : len;
     const uint32_t incl = warp_incl_scan(slen, c.lane);
     const uint32_t tot = __shfl_sync(kFull, incl, 31);
     const uint32_t excl = incl - slen;
-    if (TRACE) {
-      tr[kTrStreamElems] += tot;
-      tr[kTrSearchLists] += __popc(__ballot_sync(kFull, search));
-    }
-    uint32_t hits = 0;
-    for (uint32_t t = 0; t < tot; t += 32 * kStreamUnroll) {
-      uint32_t y[kStreamUnroll];
-      bool ok[kStreamUnroll];
+    if (TRACE) tr[kTrStreamElems] += tot;
+    for (uint32_t t = 0; t < tot; t += 32) {
+      const uint32_t idx = t + c.lane;
+      int j = 0;
 #pragma unroll
-      for (int u = 0; u < kStreamUnroll; ++u) {
-        const uint32_t idx = t + u * 32 + c.lane;
-        int j = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const uint32_t ex = __shfl_sync(kFull, excl, j + step);
-          if (ex <= idx) j += step;
-        }
-        const uint32_t o_start = __shfl_sync(kFull, start, j);
-        const uint32_t o_excl = __shfl_sync(kFull, excl, j);
-        const uint32_t o_lo = __shfl_sync(kFull, lo_val, j);
-        const uint32_t o_hi = __shfl_sync(kFull, hi_val, j);
-        const uint32_t* o_base = reinterpret_cast<const uint32_t*>(
-            __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j));
-        ok[u] = idx < tot;
-        y[u] = ok[u] ? __ldg(o_base + o_start + (idx - o_excl)) : 0u;
-        ok[u] = ok[u] && y[u] >= o_lo && y[u] < o_hi;
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t ex = __shfl_sync(kFull, excl, j + step);
+        if (ex <= idx) j += step;
       }
-#pragma unroll
-      for (int u = 0; u < kStreamUnroll; ++u)
-        if (ok[u] && probe(P, y[u])) ++hits;
+      const uint32_t o_excl = __shfl_sync(kFull, excl, j);
+      const uint32_t o_lo = __shfl_sync(kFull, lo_val, j);
+      const uint32_t o_hi = __shfl_sync(kFull, hi_val, j);
+      const uint32_t* o_base = reinterpret_cast<const uint32_t*>(
+          __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j));
+      if (idx < tot) {
+        const uint32_t y = __ldg(o_base + (idx - o_excl));
+        if (y >= o_lo && y < o_hi && probe(P, y)) ++hits;
+      }
     }
+    // 3) skewed pairs: binary-search P's elements (within the window) into N(s)
     unsigned sm = __ballot_sync(kFull, search);
     while (sm) {
       const int j = __ffs(sm) - 1;
@@ -566,7 +718,7 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
 }
 
 template <bool METER, bool TRACE>
-__global__ void __launch_bounds__(kThreads) count_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) {
   __shared__ WarpState states[kWarpsPerBlock];
   extern __shared__ uint32_t dyn_smem[];
   const int lane = threadIdx.x & 31;
@@ -581,7 +733,7 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const KernelArgs a) {
   c.cap = a.cap;
   c.lane = lane;
   c.hash = dyn_smem + wib * kHashSlots;
-  const bool batch = !METER && P.batch;
+  const bool batch = P.batch;
   HeavyQueue hq;
   hq.items = a.heavy_items;
   hq.cap = a.heavy_cap;
@@ -635,6 +787,7 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const KernelArgs a) {
         continue;
       }
       if (batch && P.depth == 4) {
+        if (METER) elems += meter_batch(c, P);
         if (TRACE) tclk = clock64();
         checked_acc(cnt, leaf_batch<TRACE>(c, P, hq, tr), ovf);
         if (TRACE) tr[kTrBatchCycles] += clock64() - tclk;
@@ -665,6 +818,7 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const KernelArgs a) {
             tr[kTrLeaves] += 1;
           }
         } else if (batch && level == P.depth - 3) {
+          if (METER) elems += meter_batch(c, P);
           if (TRACE) tclk = clock64();
           checked_acc(cnt, leaf_batch<TRACE>(c, P, hq, tr), ovf);
           if (TRACE) tr[kTrBatchCycles] += clock64() - tclk;
@@ -691,23 +845,263 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const KernelArgs a) {
   }
 }
 
-// CTA tier: the deferred batches, one per CTA at a time, with a 128 KB table
-// shared by kHeavyWarps warps.  Probe sets beyond the table are split into
-// value-range chunks (the streamed lists are range-restricted per chunk, so
-// every element is still probed exactly once).
+// ---------------------------------------------------------------- CTA tier ---
+// The deferred batches, one per CTA at a time: 16 warps share a 64 KB
+// bucketised table.  Node builds are CTA-wide two-pass filters (count per
+// warp slice, scan, write), and the leaf stream is a CTA-wide load-balanced
+// search: per tile of 512 lists a block scan of the list lengths, then every
+// thread expands kLbsRun consecutive elements of the concatenation (one owner
+// search per run, kLbsRun independent loads in flight).  Probe sets beyond
+// the table are split into value-range chunks (the streamed lists are
+// range-restricted per chunk, so every element is still probed exactly once).
+
+constexpr int kLbsRun = 8;
+constexpr int kTile = kHeavyThreads;
+
+struct HeavyShared {
+  WarpState st;
+  unsigned long long item;
+  unsigned long long red_a[kHeavyWarps], red_b[kHeavyWarps];
+  uint32_t wsum[kHeavyWarps + 1];
+  uint32_t offs[kTile + 1];
+  const uint32_t* lptr[kTile];
+  uint32_t llo[kTile], lhi[kTile];
+  uint32_t search_idx[kTile];
+  uint32_t nsearch;
+};
+
+// Block-wide exclusive scan of one value per thread; *total gets the sum.
+__device__ uint32_t cta_excl_scan(uint32_t v, HeavyShared& sh, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t incl = warp_incl_scan(v, lane);
+  if (lane == 31) sh.wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = lane < kHeavyWarps ? sh.wsum[lane] : 0u;
+    const uint32_t xi = warp_incl_scan(x, lane);
+    if (lane < kHeavyWarps) sh.wsum[lane] = xi - x;
+    if (lane == kHeavyWarps - 1) sh.wsum[kHeavyWarps] = xi;
+  }
+  __syncthreads();
+  const uint32_t r = sh.wsum[warp] + incl - v;
+  *total = sh.wsum[kHeavyWarps];
+  __syncthreads();
+  return r;
+}
+
+// Fill the CTA table with arr[0..n) (all threads; includes the syncs).
+__device__ ProbeSet cta_table(uint32_t* table, const uint32_t* arr, uint32_t n) {
+  ProbeSet p;
+  p.arr = arr;
+  p.n = n;
+  p.lo = arr[0];
+  p.hi = arr[n - 1];
+  p.hash = table;
+  p.bits = table_bits(n);
+  __syncthreads();
+  fill_table(table, p, threadIdx.x, kHeavyThreads);
+  __syncthreads();
+  insert_table(table, p, threadIdx.x, kHeavyThreads);
+  __syncthreads();
+  return p;
+}
+
+// CTA-wide build of node t (see build_node).
+__device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShared& sh,
+                               uint32_t* table) {
+  const Node& nd = P.nodes[t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* in;
+  uint32_t inlen;
+  node_input(c, nd, in, inlen);
+  if (nd.raw || nd.nops != 1) {
+    if (warp == 0) build_node(c, P, t);  // raw slice, or a multi-op start node (rare)
+    __syncthreads();
+    return;
+  }
+  uint32_t* out = c.scratch + static_cast<uint64_t>(nd.slot) * c.cap;
+  const WarpState& s = sh.st;
+  const uint32_t v = s.vals[nd.ops[0].level];
+  const uint32_t* L;
+  uint32_t nL;
+  nbrs(c, v, L, nL);
+  const uint32_t* X = in;
+  uint32_t nX = inlen;
+  ProbeSet pr;
+  pr.arr = L;
+  pr.n = 0;
+  pr.bits = 0;
+  bool keep_found = true;
+  uint32_t exclude = kEmptySlot;
+  if (inlen == 0) {
+    nX = 0;
+  } else if (nd.ops[0].mode == kOpIsect) {
+    if (nd.bound >= 0) nL = lower_bound_dev(L, nL, s.vals[nd.bound]);
+    if (nL == 0) {
+      nX = 0;
+    } else {
+      const bool in_small = inlen <= nL;
+      const uint32_t* Sm = in_small ? in : L;
+      const uint32_t nSm = in_small ? inlen : nL;
+      const uint32_t* Lg = in_small ? L : in;
+      const uint32_t nLg = in_small ? nL : inlen;
+      if (2 * nSm <= kHeavySlots && nLg >= 4 * nSm) {
+        pr = cta_table(table, Sm, nSm);
+        X = Lg;
+        nX = nLg;
+      } else if (2 * nSm <= kHeavySlots && nSm > 32) {
+        pr = cta_table(table, Sm, nSm);
+        X = Lg;
+        nX = nLg;
+      } else {
+        pr.arr = Lg;
+        pr.n = nLg;
+        pr.lo = Lg[0];
+        pr.hi = Lg[nLg - 1];
+        X = Sm;
+        nX = nSm;
+      }
+    }
+  } else {
+    keep_found = false;
+    exclude = v;
+    const uint32_t a = lower_bound_dev(L, nL, in[0]);
+    const uint32_t b = lower_bound_dev(L, nL, in[inlen - 1] + 1u);
+    if (b > a) {
+      if (2 * (b - a) <= kHeavySlots) {
+        pr = cta_table(table, L + a, b - a);
+      } else {
+        pr.arr = L + a;
+        pr.n = b - a;
+        pr.lo = pr.arr[0];
+        pr.hi = pr.arr[pr.n - 1];
+      }
+    }
+  }
+  // two passes over per-warp slices: count, scan, write in order
+  const uint32_t chunk = ((nX + kHeavyWarps - 1) / kHeavyWarps + 127) / 128 * 128;
+  const uint32_t lo = min(nX, warp * chunk), hi = min(nX, lo + chunk);
+  const uint32_t cnt = filter_list<true>(c, X + lo, hi - lo, pr, keep_found, exclude, nullptr);
+  if (lane == 0) sh.wsum[warp] = cnt;
+  __syncthreads();
+  uint32_t off = 0, total = 0;
+  for (int w = 0; w < kHeavyWarps; ++w) {
+    off += w < warp ? sh.wsum[w] : 0u;
+    total += sh.wsum[w];
+  }
+  filter_list<false>(c, X + lo, hi - lo, pr, keep_found, exclude, out + off);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sh.st.ptr[t] = out;
+    sh.st.len[t] = total;
+  }
+  __syncthreads();
+}
+
+// CTA-wide load-balanced stream: sum_{s in S} |N(s) & [lo_s, hi_s) & P|.
+// Returns this thread's partial count.
 template <bool TRACE>
-__global__ void __launch_bounds__(kHeavyThreads) heavy_kernel(const KernelArgs a) {
-  __shared__ WarpState st;
-  __shared__ unsigned long long item_sh;
-  __shared__ unsigned long long red_a[kHeavyWarps], red_b[kHeavyWarps];
-  extern __shared__ uint32_t table[];
+__device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, const ProbeSet& P,
+                               int rel, HeavyShared& sh, uint64_t* tr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t hits = 0;
+  for (uint32_t tile = 0; tile < nS; tile += kTile) {
+    const uint32_t i = tile + threadIdx.x;
+    if (threadIdx.x == 0) sh.nsearch = 0;
+    uint32_t len = 0, start = 0, lo_val = P.lo, hi_val = P.hi + 1u;
+    const uint32_t* base = c.adj;
+    if (i < nS) {
+      const uint32_t s = S[i];
+      if (rel == 1) hi_val = min(hi_val, s);
+      if (rel == 2) lo_val = max(lo_val, s + 1u);
+      const unsigned long long b = __ldg(c.off + s), e = __ldg(c.off + s + 1);
+      base = c.adj + b;
+      const uint32_t deg = static_cast<uint32_t>(e - b);
+      if (lo_val < hi_val && deg) {
+        const uint32_t first = __ldg(base), last = __ldg(base + deg - 1);
+        if (last >= lo_val && first < hi_val) {
+          uint32_t end = deg;
+          if (deg > 32) {
+            if (first < lo_val) start = lower_bound_dev(base, deg, lo_val);
+            if (last >= hi_val) end = lower_bound_dev(base, deg, hi_val);
+          }
+          len = end > start ? end - start : 0u;
+        }
+      }
+    }
+    __syncthreads();  // nsearch reset visible
+    const bool search = len > kLongList && static_cast<uint64_t>(P.n) * ilog2p1(len) * 2u < len;
+    if (search) sh.search_idx[atomicAdd(&sh.nsearch, 1u)] = threadIdx.x;
+    const uint32_t slen = search ? 0u : len;
+    uint32_t total;
+    const uint32_t off = cta_excl_scan(slen, sh, &total);
+    sh.offs[threadIdx.x] = off;
+    if (threadIdx.x == 0) sh.offs[kTile] = total;
+    sh.lptr[threadIdx.x] = base + start;
+    sh.llo[threadIdx.x] = lo_val;
+    sh.lhi[threadIdx.x] = hi_val;
+    __syncthreads();
+    if (TRACE && threadIdx.x == 0) tr[kTrStreamElems] += total;
+    for (uint32_t e0 = threadIdx.x * kLbsRun; e0 < total; e0 += kTile * kLbsRun) {
+      // owner of e0: the last j with offs[j] <= e0
+      uint32_t j = 0;
+#pragma unroll
+      for (uint32_t step = kTile / 2; step >= 1; step >>= 1)
+        if (sh.offs[j + step] <= e0) j += step;
+      uint32_t y[kLbsRun];
+      uint32_t ylo[kLbsRun], yhi[kLbsRun];
+#pragma unroll
+      for (int k = 0; k < kLbsRun; ++k) {
+        const uint32_t e = e0 + k;
+        y[k] = kEmptySlot;
+        ylo[k] = 1u;
+        yhi[k] = 0u;
+        if (e < total) {
+          while (sh.offs[j + 1] <= e) ++j;
+          y[k] = __ldg(sh.lptr[j] + (e - sh.offs[j]));
+          ylo[k] = sh.llo[j];
+          yhi[k] = sh.lhi[j];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kLbsRun; ++k)
+        if (y[k] >= ylo[k] && y[k] < yhi[k] && probe(P, y[k])) ++hits;
+    }
+    // skewed pairs: one warp per list, P's window binary-searched into N(s)
+    for (uint32_t q = warp; q < sh.nsearch; q += kHeavyWarps) {
+      const uint32_t jt = sh.search_idx[q];
+      const uint32_t* jb = sh.lptr[jt];
+      const uint32_t jl = (jt + 1 < kTile ? 0u : 0u);
+      (void)jl;
+      const uint32_t jlo = sh.llo[jt], jhi = sh.lhi[jt];
+      // the list's length was not kept in smem: recompute from its window
+      const uint32_t pa = lower_bound_rw(P.arr, P.n, jlo);
+      const uint32_t pb = lower_bound_rw(P.arr, P.n, jhi);
+      const uint32_t s = S[tile + jt];
+      const unsigned long long b = __ldg(c.off + s), e = __ldg(c.off + s + 1);
+      const uint32_t* lb = c.adj + b;
+      const uint32_t deg = static_cast<uint32_t>(e - b);
+      for (uint32_t qq = pa + lane; qq < pb; qq += 32)
+        if (contains_dev(lb, deg, P.arr[qq])) ++hits;
+      (void)jb;
+    }
+    __syncthreads();
+  }
+  return hits;
+}
+
+template <bool TRACE>
+__global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArgs a) {
+  __shared__ HeavyShared sh;
+  extern __shared__ uint4 table4[];
+  uint32_t* table = reinterpret_cast<uint32_t*>(table4);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const Program& P = a.prog;
   Ctx c;
   c.off = a.off;
   c.adj = a.adj;
-  c.s = &st;
+  c.s = &sh.st;
   c.scratch = a.heavy_scratch + static_cast<uint64_t>(blockIdx.x) * P.nslots * a.cap;
   c.cap = a.cap;
   c.lane = lane;
@@ -721,32 +1115,31 @@ __global__ void __launch_bounds__(kHeavyThreads) heavy_kernel(const KernelArgs a
   bool ovf = false;
   const bool yltx = P.batch_yltx != 0;
   for (;;) {
-    if (threadIdx.x == 0) item_sh = atomicAdd(&a.ctr->heavy_next, 1ull);
+    if (threadIdx.x == 0) sh.item = atomicAdd(&a.ctr->heavy_next, 1ull);
     __syncthreads();
-    const unsigned long long it = item_sh;
+    const unsigned long long it = sh.item;
     if (it >= nitems) break;
     long long t0 = TRACE ? clock64() : 0;
-    if (warp == 0) {
-      if (lane < P.depth - 2) st.vals[lane] = a.heavy_items[it * kHeavyItemWords + lane];
-      __syncwarp();
-      for (int t = P.node_begin[0]; t < P.node_end[P.depth - 3]; ++t) build_node(c, P, t);
-    }
+    if (threadIdx.x < P.depth - 2) sh.st.vals[threadIdx.x] = a.heavy_items[it * kHeavyItemWords + threadIdx.x];
     __syncthreads();
-    const BatchSets b = batch_sets(st, P);
+    for (int t = P.node_begin[0]; t < P.node_end[P.depth - 3]; ++t) cta_build_node(c, P, t, sh, table);
+    long long t1 = TRACE ? clock64() : 0;
+    if (TRACE && threadIdx.x == 0) tr[kTrHeavyBuild] += t1 - t0;
+    const BatchSets b = batch_sets(sh.st, P);
     // side choice from the degree sums (CTA-wide)
     bool flip = false;
     if (!b.same) {
       const uint64_t da = degree_sum(c, b.A, b.nA, warp * 32, kHeavyThreads);
       const uint64_t db = degree_sum(c, b.B, b.nB, warp * 32, kHeavyThreads);
       if (lane == 0) {
-        red_a[warp] = da;
-        red_b[warp] = db;
+        sh.red_a[warp] = da;
+        sh.red_b[warp] = db;
       }
       __syncthreads();
       uint64_t sa = 0, sb = 0;
       for (int w = 0; w < kHeavyWarps; ++w) {
-        sa += red_a[w];
-        sb += red_b[w];
+        sa += sh.red_a[w];
+        sb += sh.red_b[w];
       }
       flip = sb < sa;
       __syncthreads();
@@ -758,31 +1151,22 @@ __global__ void __launch_bounds__(kHeavyThreads) heavy_kernel(const KernelArgs a
     const int rel = yltx ? (flip ? 2 : 1) : 0;
     uint64_t core = 0;
     for (uint32_t pc = 0; pc < Pn; pc += kHeavyChunk) {
-      ProbeSet ps;
-      ps.arr = Parr + pc;
-      ps.n = min(kHeavyChunk, Pn - pc);
-      ps.lo = ps.arr[0];
-      ps.hi = ps.arr[ps.n - 1];
-      ps.hash = table;
-      ps.bits = table_bits(ps.n);
-      fill_table(table, ps, threadIdx.x, kHeavyThreads);
-      __syncthreads();
-      insert_table(table, ps, threadIdx.x, kHeavyThreads);
-      __syncthreads();
-      core += stream_count<TRACE>(c, S, nS, ps, rel, warp * 32, kHeavyWarps * 32, tr);
-      __syncthreads();
+      const ProbeSet ps = cta_table(table, Parr + pc, min(kHeavyChunk, Pn - pc));
+      core += cta_stream<TRACE>(c, S, nS, ps, rel, sh, tr);
     }
+    core = warp_sum64(core);
+    if (TRACE && threadIdx.x == 0) tr[kTrHeavyStream] += clock64() - t1;
     const uint64_t dpart = P.batch_diff ? diff_terms(c, P, b, warp * 32, kHeavyThreads, warp == 0) : 0;
     if (lane == 0) {
-      red_a[warp] = core;
-      red_b[warp] = dpart;
+      sh.red_a[warp] = core;
+      sh.red_b[warp] = dpart;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       uint64_t sc = 0, sd = 0;
       for (int w = 0; w < kHeavyWarps; ++w) {
-        sc += red_a[w];
-        sd += red_b[w];
+        sc += sh.red_a[w];
+        sd += sh.red_b[w];
       }
       checked_acc(cnt, P.batch_diff ? sd - sc : sc, ovf);
       if (TRACE) {
@@ -801,7 +1185,8 @@ __global__ void __launch_bounds__(kHeavyThreads) heavy_kernel(const KernelArgs a
   }
   if (TRACE && lane == 0) {
     for (int i = 0; i < kTrCount; ++i)
-      if (tr[i] && (i != kTrHeavyItems && i != kTrHeavyCycles || threadIdx.x == 0))
+      if (tr[i] && ((i != kTrHeavyItems && i != kTrHeavyCycles && i != kTrHeavyBuild &&
+                     i != kTrHeavyStream) || threadIdx.x == 0))
         atomicAdd(&a.ctr->trace[i], static_cast<unsigned long long>(tr[i]));
   }
 }
@@ -908,7 +1293,7 @@ struct Launch {
 template <bool METER, bool TRACE>
 int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
   const uint64_t cap = std::max<uint64_t>(32, (g.max_degree + 31) / 32 * 32);
-  const bool heavy = !METER && prog.batch;
+  const bool heavy = prog.batch != 0;
   SMG_CUDA(cudaFuncSetAttribute(count_kernel<METER, TRACE>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDynSmem)));
   int per_sm = 0;
@@ -925,7 +1310,7 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   if (heavy) {
     if (!r.heavy_items)
       SMG_CUDA(cudaMalloc(&r.heavy_items, kHeavyQueueCap * kHeavyItemWords * sizeof(uint32_t)));
-    const size_t hs = static_cast<size_t>(r.num_sms) * prog.nslots * cap * 4;
+    const size_t hs = static_cast<size_t>(r.num_sms) * 4 * prog.nslots * cap * 4;  // <= 4 CTAs/SM
     if (r.heavy_scratch_bytes < hs) {
       if (r.heavy_scratch) cudaFree(r.heavy_scratch);
       r.heavy_scratch = nullptr;
@@ -962,7 +1347,11 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
     if (heavy) {
       SMG_CUDA(cudaFuncSetAttribute(heavy_kernel<TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kHeavySmem)));
-      heavy_kernel<TRACE><<<r.num_sms, kHeavyThreads, kHeavySmem, st>>>(a);
+      int hper = 0;
+      SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hper, heavy_kernel<TRACE>, kHeavyThreads,
+                                                             kHeavySmem));
+      hper = std::max(1, hper);
+      heavy_kernel<TRACE><<<r.num_sms * hper, kHeavyThreads, kHeavySmem, st>>>(a);
     }
   }
   SMG_CUDA(cudaGetLastError());
@@ -992,7 +1381,8 @@ int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* 
                                           "batches_hashed", "stream_elems", "search_lists",
                                           "probe_set_sum", "stream_set_sum", "leaf_cycles",
                                           "leaves", "bigP_stream_cycles", "deferred",
-                                          "heavy_items", "heavy_cycles"};
+                                          "heavy_items", "heavy_cycles", "long_lists",
+                                          "heavy_build_cycles", "heavy_stream_cycles"};
     std::fprintf(stderr, "[smg trace] kernel %.3f ms:", t);
     for (int i = 0; i < kTrCount; ++i)
       std::fprintf(stderr, " %s=%.4g", names[i], static_cast<double>(r.host_ctr->trace[i]));
