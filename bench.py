@@ -228,6 +228,16 @@ def load_traffic():
         return None
 
 
+def kernels_per_count(plan) -> int:
+    """count_kernel, plus heavy_kernel when the plan's leaf is batched."""
+    import ctypes
+    from paper_1911_12877_b200 import _native as N
+    sp = plan.to_smg()
+    buf = ctypes.create_string_buffer(1 << 16)
+    N.check_gpu(N.gpu_lib().smg_plan_describe(ctypes.byref(sp), buf, 1 << 16))
+    return 2 if json.loads(buf.value.decode())["batch"] else 1
+
+
 def our_arm(args):
     import ctypes
     import numpy as np
@@ -384,7 +394,7 @@ def our_arm(args):
                          "kernel": f"count_kernel<false> ({dom})", "peak_source": peak_kind,
                          "note": "achieved = 4 B x E (algorithmic, merge-based) / kernel time; "
                                  "hoisting and probe-side selection read far fewer bytes"},
-            "gpu_launches": args.steps * len(plans),
+            "gpu_launches": args.steps * sum(kernels_per_count(p) for _, p in plans),
             "clocks": clocks.summary(),
         }
         if cpu:

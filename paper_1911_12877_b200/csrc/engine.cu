@@ -60,7 +60,7 @@ struct Counters {
   unsigned long long heavy_count;  // batches deferred to the CTA tier
   unsigned long long heavy_next;   // CTA-tier queue cursor
   unsigned int overflow;
-  unsigned int pad;
+  unsigned int heavy_done;         // CTAs of heavy_kernel finished
   // SMG_TRACE=1: per-phase cycle and event counters (see kTr* below)
   unsigned long long trace[32];  // >= kTrCount
 };
@@ -1182,6 +1182,13 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
       if (old + cnt < old) ovf = true;
     }
     if (ovf) atomicOr(&a.ctr->overflow, 1u);
+    // the last CTA out rewinds the queue cursor, so a replay of this launch
+    // (profiler kernel replay) sees the same queue
+    __threadfence();
+    if (atomicAdd(&a.ctr->heavy_done, 1u) == gridDim.x - 1) {
+      a.ctr->heavy_next = 0;
+      a.ctr->heavy_done = 0;
+    }
   }
   if (TRACE && lane == 0) {
     for (int i = 0; i < kTrCount; ++i)
