@@ -92,6 +92,27 @@ typedef struct smg_graph smg_graph;
 int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_t n_vertices,
                      const int* devices, int num_devices, smg_graph** out);
 void smg_graph_destroy(smg_graph* g);
+
+/*
+ * Graph::from_edges (graph.cpp:13-47) on the device: pairs[2i], pairs[2i+1]
+ * is edge i over vertices 0..n-1; self loops and duplicates are dropped and
+ * counted (LoadStats, graph.hpp:13-16); the sorted symmetric CSR is built on
+ * devices[0] (radix sorts) and replicated on the others.  The result is
+ * structurally equal (Graph::operator==, graph.hpp:50-52) to the host build.
+ */
+int smg_graph_from_edges(const uint32_t* pairs, uint64_t num_edges, uint64_t n_vertices,
+                         const int* devices, int num_devices, smg_graph** out,
+                         uint64_t* duplicate_edges, uint64_t* self_loops);
+
+/*
+ * orient_reindex (graph.cpp:137-161) on replica `replica`'s device: new ids by
+ * (degree desc, old id asc); new_to_old (n entries, host) may be NULL.  The new
+ * graph has one replica on that device.
+ */
+int smg_graph_orient(const smg_graph* g, int replica, smg_graph** out, uint32_t* new_to_old);
+
+/* Copy replica `replica`'s CSR to the host (offsets: n+1, adjacency: slots). */
+int smg_graph_download(const smg_graph* g, int replica, uint64_t* offsets, uint32_t* adjacency);
 int smg_graph_info(const smg_graph* g, uint64_t* n_vertices, uint64_t* n_slots,
                    uint64_t* max_degree, int* num_devices);
 

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/symmine_gpu.h"
+#include "graph_build.hpp"
 #include "program.hpp"
 
 namespace smg {
@@ -562,39 +563,53 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
     const uint32_t tot = __shfl_sync(kFull, incl, 31);
     const uint32_t excl = incl - slen;
     if (TRACE) tr[kTrStreamElems] += tot;
-    for (uint32_t t = 0; t < tot; t += 32) {
+    for (uint32_t t = 0; t < tot; t += 64) {
+      uint32_t y[2], ylo[2], yhi[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t idx = t + u * 32 + c.lane;
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const uint32_t ex = __shfl_sync(kFull, excl, j + step);
+          if (ex <= idx) j += step;
+        }
+        const uint32_t o_excl = __shfl_sync(kFull, excl, j);
+        ylo[u] = __shfl_sync(kFull, lo_val, j);
+        yhi[u] = __shfl_sync(kFull, hi_val, j);
+        const uint32_t* o_base = reinterpret_cast<const uint32_t*>(
+            __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j));
+        y[u] = idx < tot ? __ldg(o_base + (idx - o_excl)) : kEmptySlot;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (y[u] >= ylo[u] && y[u] < yhi[u] && probe(P, y[u])) ++hits;
+    }
+    // 3) skewed pairs: the (list, element of P's window) pairs are flattened
+    //    over the lanes; every lane binary-searches one element into its list
+    uint32_t pa = 0, npairs = 0;
+    if (search) {
+      pa = lower_bound_rw(P.arr, P.n, lo_val);
+      npairs = lower_bound_rw(P.arr, P.n, hi_val) - pa;
+    }
+    const uint32_t pincl = warp_incl_scan(npairs, c.lane);
+    const uint32_t ptot = __shfl_sync(kFull, pincl, 31);
+    const uint32_t pexcl = pincl - npairs;
+    for (uint32_t t = 0; t < ptot; t += 32) {
       const uint32_t idx = t + c.lane;
       int j = 0;
 #pragma unroll
       for (int step = 16; step >= 1; step >>= 1) {
-        const uint32_t ex = __shfl_sync(kFull, excl, j + step);
+        const uint32_t ex = __shfl_sync(kFull, pexcl, j + step);
         if (ex <= idx) j += step;
       }
-      const uint32_t o_excl = __shfl_sync(kFull, excl, j);
-      const uint32_t o_lo = __shfl_sync(kFull, lo_val, j);
-      const uint32_t o_hi = __shfl_sync(kFull, hi_val, j);
-      const uint32_t* o_base = reinterpret_cast<const uint32_t*>(
-          __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j));
-      if (idx < tot) {
-        const uint32_t y = __ldg(o_base + (idx - o_excl));
-        if (y >= o_lo && y < o_hi && probe(P, y)) ++hits;
-      }
-    }
-    // 3) skewed pairs: binary-search P's elements (within the window) into N(s)
-    unsigned sm = __ballot_sync(kFull, search);
-    while (sm) {
-      const int j = __ffs(sm) - 1;
-      sm &= sm - 1;
-      const uint32_t* jb = reinterpret_cast<const uint32_t*>(
-          __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j));
-      const uint32_t js = __shfl_sync(kFull, start, j);
-      const uint32_t jl = __shfl_sync(kFull, len, j);
-      const uint32_t jlo = __shfl_sync(kFull, lo_val, j);
-      const uint32_t jhi = __shfl_sync(kFull, hi_val, j);
-      const uint32_t pa = lower_bound_rw(P.arr, P.n, jlo);
-      const uint32_t pb = lower_bound_rw(P.arr, P.n, jhi);
-      for (uint32_t q = pa + c.lane; q < pb; q += 32)
-        if (contains_dev(jb + js, jl, P.arr[q])) ++hits;
+      const uint32_t o_pa = __shfl_sync(kFull, pa, j);
+      const uint32_t o_ex = __shfl_sync(kFull, pexcl, j);
+      const uint32_t o_len = __shfl_sync(kFull, len, j);
+      const uint32_t* o_list = reinterpret_cast<const uint32_t*>(
+                                   __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j)) +
+                               __shfl_sync(kFull, start, j);
+      if (idx < ptot && contains_dev(o_list, o_len, P.arr[o_pa + (idx - o_ex)])) ++hits;
     }
     total += hits;
   }
@@ -1043,24 +1058,33 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
     __syncthreads();
     if (TRACE && threadIdx.x == 0) tr[kTrStreamElems] += total;
     for (uint32_t e0 = threadIdx.x * kLbsRun; e0 < total; e0 += kTile * kLbsRun) {
-      // owner of e0: the last j with offs[j] <= e0
+      // owner of e0: the last j with offs[j] <= e0; its list state is kept in
+      // registers and reloaded only when the run crosses into the next list
       uint32_t j = 0;
 #pragma unroll
       for (uint32_t step = kTile / 2; step >= 1; step >>= 1)
         if (sh.offs[j + step] <= e0) j += step;
+      const uint32_t* lp = sh.lptr[j] - sh.offs[j];
+      uint32_t lo = sh.llo[j], hi = sh.lhi[j], next = sh.offs[j + 1];
       uint32_t y[kLbsRun];
       uint32_t ylo[kLbsRun], yhi[kLbsRun];
 #pragma unroll
       for (int k = 0; k < kLbsRun; ++k) {
         const uint32_t e = e0 + k;
         y[k] = kEmptySlot;
-        ylo[k] = 1u;
-        yhi[k] = 0u;
+        ylo[k] = lo;
+        yhi[k] = hi;
         if (e < total) {
-          while (sh.offs[j + 1] <= e) ++j;
-          y[k] = __ldg(sh.lptr[j] + (e - sh.offs[j]));
-          ylo[k] = sh.llo[j];
-          yhi[k] = sh.lhi[j];
+          while (next <= e) {
+            ++j;
+            lp = sh.lptr[j] - sh.offs[j];
+            lo = sh.llo[j];
+            hi = sh.lhi[j];
+            next = sh.offs[j + 1];
+          }
+          y[k] = __ldg(lp + e);
+          ylo[k] = lo;
+          yhi[k] = hi;
         }
       }
 #pragma unroll
@@ -1555,6 +1579,128 @@ int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_
     }
   }
   *out = g;
+  return SMG_OK;
+}
+
+// Runtime parts of a replica (stream, events, counters) on `dev`.
+static int init_replica_runtime(Replica* r, int dev) {
+  r->device = dev;
+  SMG_CUDA(cudaSetDevice(dev));
+  SMG_CUDA(cudaDeviceGetAttribute(&r->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  SMG_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+  SMG_CUDA(cudaEventCreate(&r->ev0));
+  SMG_CUDA(cudaEventCreate(&r->ev1));
+  SMG_CUDA(cudaMalloc(&r->ctr, sizeof(Counters)));
+  SMG_CUDA(cudaMallocHost(&r->host_ctr, sizeof(Counters)));
+  return SMG_OK;
+}
+
+// Wrap a device CSR built on devs[0] into a graph replicated on devs.
+static int adopt_device_csr(const DevCSR& csr, const int* devs, int ndevs, smg_graph** out) {
+  smg_graph* g = new smg_graph;
+  g->n = csr.n;
+  g->slots = csr.slots;
+  g->max_degree = csr.max_degree;
+  for (int i = 0; i < ndevs; ++i) {
+    Replica* r = new Replica;
+    g->reps.push_back(r);
+    int rc = init_replica_runtime(r, devs[i]);
+    if (rc) {
+      if (i == 0) {  // still owns the arrays
+        cudaFree(csr.off);
+        cudaFree(csr.adj);
+        cudaFree(csr.src);
+      }
+      smg_graph_destroy(g);
+      return rc;
+    }
+    if (i == 0) {
+      r->off = csr.off;
+      r->adj = csr.adj;
+      r->src = csr.src;
+      continue;
+    }
+    const size_t ob = (csr.n + 1) * sizeof(unsigned long long), sb = std::max<uint64_t>(csr.slots, 1) * 4;
+    cudaError_t e = cudaMalloc(&r->off, ob);
+    if (e == cudaSuccess) e = cudaMalloc(&r->adj, sb);
+    if (e == cudaSuccess) e = cudaMalloc(&r->src, sb);
+    // UVA: device-to-device (NVLink peer path where enabled)
+    if (e == cudaSuccess) e = cudaMemcpy(r->off, csr.off, ob, cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(r->adj, csr.adj, sb, cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(r->src, csr.src, sb, cudaMemcpyDefault);
+    if (e != cudaSuccess) {
+      smg_graph_destroy(g);
+      return fail(SMG_EIO, std::string("replicate CSR: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = g;
+  return SMG_OK;
+}
+
+int smg_graph_from_edges(const uint32_t* pairs, uint64_t num_edges, uint64_t n, const int* devices,
+                         int num_devices, smg_graph** out, uint64_t* dups, uint64_t* loops) {
+  if (!out) return fail(SMG_EINPUT, "null output handle");
+  *out = nullptr;
+  if (n >= (1ull << 32)) return fail(SMG_EINPUT, "vertex ids must fit in 32 bits");
+  if (num_edges && !pairs) return fail(SMG_EINPUT, "null edge array");
+  if (num_devices < 1 || num_devices > SMG_MAX_GPUS) return fail(SMG_EINPUT, "num_devices must be 1..8");
+  const int ndev = smg_device_count();
+  if (ndev == 0) return fail(SMG_EIO, "no CUDA device available (the engine has no CPU path)");
+  int devs[SMG_MAX_GPUS];
+  for (int i = 0; i < num_devices; ++i) {
+    devs[i] = devices ? devices[i] : i;
+    if (devs[i] < 0 || devs[i] >= ndev) return fail(SMG_EINPUT, "device index out of range");
+  }
+  Replica tmp;
+  int rc = init_replica_runtime(&tmp, devs[0]);
+  if (rc) return rc;
+  DevCSR csr;
+  uint64_t d = 0, l = 0;
+  std::string err;
+  rc = device_from_edges(devs[0], tmp.stream, tmp.num_sms, pairs, num_edges, n, &csr, &d, &l, &err);
+  cudaStreamDestroy(tmp.stream);
+  cudaEventDestroy(tmp.ev0);
+  cudaEventDestroy(tmp.ev1);
+  cudaFree(tmp.ctr);
+  cudaFreeHost(tmp.host_ctr);
+  tmp.stream = nullptr;
+  if (rc) return fail(rc == 2 ? SMG_EINPUT : SMG_EIO, err);
+  if (dups) *dups = d;
+  if (loops) *loops = l;
+  return adopt_device_csr(csr, devs, num_devices, out);
+}
+
+int smg_graph_orient(const smg_graph* g, int replica, smg_graph** out, uint32_t* new_to_old) {
+  if (!g || !out) return fail(SMG_EINPUT, "null argument");
+  *out = nullptr;
+  if (replica < 0 || replica >= static_cast<int>(g->reps.size())) return fail(SMG_EINPUT, "bad replica");
+  Replica& r = *g->reps[replica];
+  std::lock_guard<std::mutex> lock(r.mu);
+  DevCSR in;
+  in.off = r.off;
+  in.adj = r.adj;
+  in.src = r.src;
+  in.n = g->n;
+  in.slots = g->slots;
+  in.max_degree = g->max_degree;
+  DevCSR o;
+  std::string err;
+  const int rc = device_orient(r.device, r.stream, r.num_sms, in, &o, new_to_old, &err);
+  if (rc) return fail(SMG_EIO, err);
+  const int dev = r.device;
+  return adopt_device_csr(o, &dev, 1, out);
+}
+
+int smg_graph_download(const smg_graph* g, int replica, uint64_t* offsets, uint32_t* adjacency) {
+  if (!g || !offsets) return fail(SMG_EINPUT, "null argument");
+  if (replica < 0 || replica >= static_cast<int>(g->reps.size())) return fail(SMG_EINPUT, "bad replica");
+  const Replica& r = *g->reps[replica];
+  SMG_CUDA(cudaSetDevice(r.device));
+  SMG_CUDA(cudaMemcpy(offsets, r.off, (g->n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (g->slots) {
+    if (!adjacency) return fail(SMG_EINPUT, "null adjacency");
+    SMG_CUDA(cudaMemcpy(adjacency, r.adj, g->slots * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  }
   return SMG_OK;
 }
 

@@ -151,6 +151,51 @@ class Graph:
             pass
 
 
+def _adopt_device(h, device: int) -> Graph:
+    """Download a device-built graph handle and keep it as the Graph's replica."""
+    lib = N.gpu_lib()
+    n, s, m, nd = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int()
+    N.check_gpu(lib.smg_graph_info(h, ctypes.byref(n), ctypes.byref(s), ctypes.byref(m),
+                                   ctypes.byref(nd)))
+    off = np.zeros(n.value + 1, dtype=np.uint64)
+    adj = np.zeros(max(s.value, 1), dtype=np.uint32)
+    N.check_gpu(lib.smg_graph_download(h, 0, off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                       adj.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+    g = Graph(off, adj[: s.value], check=False)
+    g._dev[(device,)] = h
+    return g
+
+
+def from_edges_device(n: int, edges, device: int = 0) -> Graph:
+    """Graph::from_edges (graph.cpp:13-47) built on the GPU (radix sorts);
+    structurally equal to Graph.from_edges.  The device copy is kept."""
+    pairs = np.ascontiguousarray(np.asarray(edges, dtype=np.int64).reshape(-1, 2))
+    if pairs.size and (pairs.min() < 0 or pairs.max() >= n):
+        raise N.InputError("edge endpoint out of range")
+    pairs = pairs.astype(np.uint32)
+    lib = N.gpu_lib()
+    h = ctypes.c_void_p()
+    d, s = ctypes.c_uint64(), ctypes.c_uint64()
+    dev = (ctypes.c_int * 1)(device)
+    ptr = pairs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)) if pairs.size else None
+    N.check_gpu(lib.smg_graph_from_edges(ptr, pairs.shape[0], n, dev, 1, ctypes.byref(h),
+                                         ctypes.byref(d), ctypes.byref(s)))
+    g = _adopt_device(h, device)
+    g.duplicate_edges, g.self_loops = d.value, s.value
+    return g
+
+
+def orient_device(g: Graph, device: int = 0):
+    """orient_reindex (graph.cpp:137-161) on the GPU -> (Graph, new_to_old)."""
+    lib = N.gpu_lib()
+    src = g.device_handle((device,))
+    h = ctypes.c_void_p()
+    n2o = np.zeros(max(g.n, 1), dtype=np.uint32)
+    N.check_gpu(lib.smg_graph_orient(src, 0, ctypes.byref(h),
+                                     n2o.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+    return _adopt_device(h, device), n2o[: g.n]
+
+
 def _check_csr(off: np.ndarray, adj: np.ndarray) -> None:
     n = off.size - 1
     if int(off[0]) != 0 or int(off[-1]) != adj.size:

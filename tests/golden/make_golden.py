@@ -150,10 +150,46 @@ def make_configs(ref: Reference, budget_s: float = 600.0) -> dict:
     return out
 
 
+def make_big_configs(ref: Reference, cfgs=("cfg3", "cfg4", "cfg5"), roots_per_pattern=48,
+                     max_deg=64, threads=None) -> dict:
+    """Reference per-root counts (Executor::count_range(v, v+1)) on seeded
+    roots of the large configs, for root-sampled GPU parity.  Roots are drawn
+    among vertices of degree <= max_deg so every reference call stays short."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_1911_12877_b200 import configs
+    threads = threads or os.cpu_count() or 1
+    out = {}
+    for cfg in cfgs:
+        t0 = time.time()
+        g = configs.load(cfg, verbose=True)
+        rg = ref.graph_from_csr(g.offsets, g.adjacency)
+        deg = np.diff(g.offsets)
+        entry = {"spec": configs.SPECS[cfg].tag, "n": g.n, "m": g.m, "max_degree": g.max_degree,
+                 "digest": csr_digest(g.offsets, g.adjacency), "roots": {}}
+        rng = np.random.default_rng(777)
+        pool = np.flatnonzero((deg > 0) & (deg <= max_deg))
+        roots = sorted(int(v) for v in rng.choice(pool, size=roots_per_pattern, replace=False))
+        for label, plan in configs.config_patterns(cfg):
+            pj = plan.to_json()
+            with ThreadPoolExecutor(max_workers=threads) as ex:
+                counts = list(ex.map(lambda v: rg.count_range(pj, v, v + 1), roots))
+            entry["roots"][label] = {"roots": roots, "counts": counts}
+            print(cfg, label, "sum", sum(counts), f"{time.time() - t0:.1f}s", flush=True)
+        out[cfg] = entry
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", action="store_true")
+    ap.add_argument("--big", action="store_true", help="cfg3-5 root samples (slow)")
     args = ap.parse_args()
+    if args.big:
+        big = make_big_configs(Reference())
+        with open(os.path.join(HERE, "configs_big.json"), "w") as f:
+            json.dump(big, f, indent=1)
+        print("configs_big.json written")
+        return
     ref = Reference()
     t = time.time()
     corpus = make_corpus(ref)

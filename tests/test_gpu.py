@@ -160,6 +160,90 @@ def test_cfg2_full_size_invariants(cfg2):
     assert count(cfg2, tri.with_options(False, True)) == 6 * count(cfg2, tri)
 
 
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+def test_big_config_reference_roots(cfg):
+    """Reference per-root counts on seeded roots of the large configs
+    (tests/golden/configs_big.json, make_golden.py --big)."""
+    import json
+    import os
+    from common import GOLDEN
+    path = os.path.join(GOLDEN, "configs_big.json")
+    if not os.path.exists(path):
+        pytest.skip("configs_big.json not generated")
+    with open(path) as f:
+        gold = json.load(f)
+    if cfg not in gold:
+        pytest.skip(f"{cfg} not in configs_big.json")
+    g = configs.load(cfg)
+    assert (g.n, g.m, g.max_degree) == (gold[cfg]["n"], gold[cfg]["m"], gold[cfg]["max_degree"])
+    for label, plan in configs.config_patterns(cfg):
+        rec = gold[cfg]["roots"].get(label)
+        if rec is None:
+            continue
+        got = [count_range(g, plan, v, v + 1).count for v in rec["roots"]]
+        assert got == rec["counts"], (cfg, label)
+
+
+def _digest(off, adj):
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(off, dtype=np.uint64).tobytes())
+    h.update(np.ascontiguousarray(adj, dtype=np.uint32).tobytes())
+    return h.hexdigest()
+
+
+def test_device_from_edges_matches_reference_layout(golden):
+    """f2: Graph::from_edges on the GPU == the reference's layout (golden sha256)."""
+    from paper_1911_12877_b200.graph import from_edges_device
+    for name, gdesc in golden["graphs"].items():
+        g = from_edges_device(gdesc["n"], gdesc["edges"])
+        assert _digest(g.offsets, g.adjacency) == golden["csr"][name]["digest"], name
+    # duplicate / self-loop statistics (SPEC.md example)
+    g = from_edges_device(3, [(0, 1), (1, 0), (0, 0), (0, 2)])
+    assert (g.duplicate_edges, g.self_loops) == (1, 1)
+    assert g.offsets.tolist() == [0, 2, 3, 4] and g.adjacency.tolist() == [1, 2, 0, 0]
+    with pytest.raises(InputError):
+        from_edges_device(3, [(0, 3)])
+
+
+def test_device_from_edges_cfg2_shuffled(golden_configs, cfg2):
+    """f2 at full size: shuffled, duplicated edges with self loops rebuild the
+    pinned cfg2 CSR exactly, and count the same."""
+    from paper_1911_12877_b200.graph import from_edges_device
+    src = np.repeat(np.arange(cfg2.n, dtype=np.uint32), np.diff(cfg2.offsets).astype(np.int64))
+    pairs = np.stack([src, cfg2.adjacency], axis=1)            # both directions
+    rng = np.random.default_rng(5)
+    pairs = pairs[rng.permutation(len(pairs))]
+    loops = np.stack([np.arange(1000, dtype=np.uint32)] * 2, axis=1)
+    pairs = np.concatenate([pairs, loops, pairs[:1000]])
+    g = from_edges_device(cfg2.n, pairs)
+    assert _digest(g.offsets, g.adjacency) == golden_configs["cfg2"]["digest"]
+    assert g.self_loops == 1000 and g.duplicate_edges == cfg2.m + 1000
+    p = named_plan("clique", 4)
+    assert count(g, p) == count(cfg2, p)
+
+
+def test_device_orient_matches_reference(golden):
+    """f1: orient_reindex on the GPU == the host/reference relabelling."""
+    from paper_1911_12877_b200.graph import orient_device
+    for name in ("K23", "petersen", "star3", "er_30_0.3_2030", "er_30_0.6_3030", "empty4"):
+        gdesc = golden["graphs"][name]
+        g = Graph.from_edges(gdesc["n"], gdesc["edges"])
+        want, want_map = g.orient_with_map()
+        got, got_map = orient_device(g)
+        assert got == want and got_map.tolist() == want_map.tolist(), name
+
+
+def test_device_orient_cfg2(cfg2):
+    from paper_1911_12877_b200.graph import orient_device
+    got, n2o = orient_device(cfg2)
+    want, want_map = cfg2.orient_with_map()
+    assert got == want and np.array_equal(n2o, want_map)
+    deg = np.diff(got.offsets)
+    assert (deg[:-1] >= deg[1:]).all()
+    assert count(got, named_plan("clique", 4)) == count(cfg2, named_plan("clique", 4))
+
+
 def test_cpp_adapter_drop_in():
     """include/symmine_gpu.hpp used from C++ with the reference's own front end
     and engine (binary built in the dev container by `make -C oracle adapter`)."""
