@@ -154,6 +154,16 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
 int smg_count_range(const smg_graph* g, const smg_plan* plan, int replica, uint32_t lo,
                     uint32_t hi, uint32_t flags, smg_result* out);
 
+/*
+ * enumerate_instances(g, plan, limit) (engine.hpp:34-37, engine.cpp:181-191):
+ * the completed embeddings as per-level vertex tuples in the reference's
+ * order (level-0 ascending, then lexicographic), truncated at `limit` when
+ * has_limit (limit 0 -> none).  Writes min(total, cap_tuples) tuples of
+ * plan->depth uint32 each to out; *n_out = total (after truncation).
+ */
+int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has_limit,
+                  uint64_t limit, uint32_t* out, uint64_t cap_tuples, uint64_t* n_out);
+
 /* Last error message of the calling thread ("" if none). */
 const char* smg_last_error(void);
 

@@ -13,14 +13,14 @@ and executes it with hand-written CUDA for sm_100a:
 """
 from ._native import CountOverflowError, InputError, IoError
 from .engine import (CountResult, count, count_pattern, count_range, count_result, count_shard,
-                     device_count, motif_counts)
+                     device_count, enumerate, motif_counts)
 from .graph import Graph
 from .plan import Plan, PlanLevel, compile_plan, motif_plans, named_plan
 
 __all__ = [
     "CountOverflowError", "CountResult", "Graph", "InputError", "IoError", "Plan", "PlanLevel",
     "compile_plan", "count", "count_pattern", "count_range", "count_result", "count_shard",
-    "device_count", "motif_counts", "motif_plans", "named_plan",
+    "device_count", "enumerate", "motif_counts", "motif_plans", "named_plan",
 ]
 
 __version__ = "0.1.0"

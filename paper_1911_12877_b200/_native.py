@@ -100,6 +100,9 @@ def gpu_lib():
                    ctypes.POINTER(_P), _U64P, _U64P])
             _bind(lib, "smg_graph_orient", ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_P), _U32P])
             _bind(lib, "smg_graph_download", ctypes.c_int, [_P, ctypes.c_int, _U64P, _U32P])
+            _bind(lib, "smg_enumerate", ctypes.c_int,
+                  [_P, ctypes.POINTER(SmgPlan), ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _U32P,
+                   ctypes.c_uint64, _U64P])
             _bind(lib, "smg_graph_set_stream", ctypes.c_int, [_P, ctypes.c_int, _P])
             _bind(lib, "smg_graph_info", ctypes.c_int,
                   [_P, _U64P, _U64P, _U64P, ctypes.POINTER(ctypes.c_int)])

@@ -18,6 +18,7 @@
 // last source vertex is fixed and reused by every deeper sibling.
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -1222,6 +1223,115 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
   }
 }
 
+// ------------------------------------------------------------- listing ---
+// enumerate_instances (engine.cpp:181-191, enumerate_from :117-134): the same
+// depth-first nested loops without leaf batching.  The reference emits in
+// level-0 ascending, then lexicographic order; edge units in CSR slot order
+// are exactly (v0 asc, v1 asc) and every candidate set is sorted, so a unit's
+// embeddings are contiguous in the global order.  Pass COUNT stores each
+// unit's embedding count; after a scan, pass WRITE writes each unit's tuples
+// at its offset, dropping those at or beyond `limit`.
+template <bool WRITE>
+__global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint64_t slot_lo,
+                                                        uint64_t slot_hi,
+                                                        unsigned long long* unit_val,
+                                                        unsigned long long limit, uint32_t* out) {
+  __shared__ WarpState states[kWarpsPerBlock];
+  extern __shared__ uint32_t dyn_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + wib;
+  const Program& P = a.prog;
+  Ctx c;
+  c.off = a.off;
+  c.adj = a.adj;
+  c.s = &states[wib];
+  c.scratch = a.scratch + gw * static_cast<uint64_t>(P.nslots + 1) * a.cap;
+  c.cap = a.cap;
+  c.lane = lane;
+  c.hash = dyn_smem + wib * kHashSlots;
+  uint32_t* leafbuf = c.scratch + static_cast<uint64_t>(P.nslots) * a.cap;
+  WarpState& s = states[wib];
+  const int n = P.depth;
+  uint32_t pos[kMaxLevels];
+  for (;;) {
+    unsigned long long e = 0;
+    if (lane == 0) e = slot_lo + atomicAdd(&a.ctr->next_chunk, 1ull);
+    e = __shfl_sync(kFull, e, 0);
+    if (e >= slot_hi) break;
+    const uint32_t v0 = __ldg(a.src + e), v1 = __ldg(a.adj + e);
+    const bool valid = !P.unit_bound || v1 < v0;
+    unsigned long long base = WRITE ? unit_val[e - slot_lo] : 0ull;
+    if (!valid || (WRITE && base >= limit)) {
+      if (!WRITE && lane == 0) unit_val[e - slot_lo] = 0;
+      continue;
+    }
+    unsigned long long written = 0;
+    if (lane == 0) {
+      s.vals[0] = v0;
+      s.vals[1] = v1;
+    }
+    __syncwarp();
+    auto emit_leaf = [&]() {
+      // materialise the leaf set, then (WRITE) its tuples
+      const uint32_t* in;
+      uint32_t inlen;
+      node_input(c, P.leaf, in, inlen);
+      const uint32_t len = apply_ops<false>(c, P.leaf, in, inlen, leafbuf);
+      __syncwarp();
+      if (WRITE) {
+        for (uint32_t i = lane; i < len; i += 32) {
+          const unsigned long long idx = base + written + i;
+          if (idx < limit) {
+            uint32_t* t = out + idx * n;
+            for (int j = 0; j < n - 1; ++j) t[j] = s.vals[j];
+            t[n - 1] = leafbuf[i];
+          }
+        }
+      }
+      written += len;
+      __syncwarp();
+    };
+    if (n == 2) {
+      if (WRITE && lane == 0 && base < limit) {
+        out[base * 2] = v0;
+        out[base * 2 + 1] = v1;
+      }
+      written = 1;
+    } else {
+      for (int t = P.node_begin[0]; t < P.node_end[0]; ++t) build_node(c, P, t);
+      for (int t = P.node_begin[1]; t < P.node_end[1]; ++t) build_node(c, P, t);
+      if (n == 3) {
+        emit_leaf();
+      } else {
+        int level = 2;
+        pos[2] = 0;
+        while (level >= 2) {
+          if (WRITE && base + written >= limit) break;
+          const int cn = P.cand[level];
+          if (pos[level] >= s.len[cn]) {
+            --level;
+            continue;
+          }
+          const uint32_t x = s.ptr[cn][pos[level]];
+          ++pos[level];
+          __syncwarp();
+          if (lane == 0) s.vals[level] = x;
+          __syncwarp();
+          for (int t = P.node_begin[level]; t < P.node_end[level]; ++t) build_node(c, P, t);
+          if (level == n - 2) {
+            emit_leaf();
+          } else {
+            ++level;
+            pos[level] = 0;
+          }
+        }
+      }
+    }
+    if (!WRITE && lane == 0) unit_val[e - slot_lo] = written;
+  }
+}
+
 // E of level 1 over roots [lo, hi): |{x in N(v0) : x < beta_1}|.
 __global__ void meter_roots_kernel(const unsigned long long* __restrict__ off,
                                    const uint32_t* __restrict__ adj, uint32_t lo, uint32_t hi,
@@ -1758,6 +1868,99 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
   out->wall_ms = now_ms() - t0;
   if (ovf) return fail(SMG_EOVERFLOW, "embedding count exceeds 64 bits");
   return SMG_OK;
+}
+
+int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has_limit,
+                  uint64_t limit, uint32_t* out, uint64_t cap_tuples, uint64_t* n_out) {
+  if (!n_out) return fail(SMG_EINPUT, "null n_out");
+  *n_out = 0;
+  Program prog;
+  int rc = prepare(g, plan, &prog);
+  if (rc) return rc;
+  if (replica < 0 || replica >= static_cast<int>(g->reps.size())) return fail(SMG_EINPUT, "bad replica");
+  if (has_limit && limit == 0) return SMG_OK;  // engine.cpp:184
+  const unsigned long long lim = has_limit ? limit : ~0ull;
+  Replica& r = *g->reps[replica];
+  std::lock_guard<std::mutex> lock(r.mu);
+  SMG_CUDA(cudaSetDevice(r.device));
+  cudaStream_t st = r.active();
+  const uint64_t cap = std::max<uint64_t>(32, (g->max_degree + 31) / 32 * 32);
+  SMG_CUDA(cudaFuncSetAttribute(enum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kDynSmem)));
+  SMG_CUDA(cudaFuncSetAttribute(enum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kDynSmem)));
+  const uint64_t blocks = static_cast<uint64_t>(r.num_sms) * 2;
+  rc = ensure_scratch(r, (prog.nslots + 1) * cap * 4 * kWarpsPerBlock * blocks);
+  if (rc) return rc;
+  const uint64_t kSlotChunk = 1ull << 22;
+  unsigned long long *uval = nullptr, *uoff = nullptr, *dtot = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  SMG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, uval, uoff, kSlotChunk + 1, st));
+  SMG_CUDA(cudaMalloc(&uval, (kSlotChunk + 1) * sizeof(unsigned long long)));
+  SMG_CUDA(cudaMalloc(&uoff, (kSlotChunk + 1) * sizeof(unsigned long long)));
+  SMG_CUDA(cudaMalloc(&tmp, tmp_bytes));
+  uint32_t* dout = nullptr;
+  size_t dout_cap = 0;
+  (void)dtot;
+  KernelArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.off = r.off;
+  a.adj = r.adj;
+  a.src = r.src;
+  a.scratch = r.scratch;
+  a.cap = cap;
+  a.ctr = r.ctr;
+  a.prog = prog;
+  unsigned long long total = 0;
+  int status = SMG_OK;
+  for (uint64_t lo = 0; lo < g->slots && total < lim && status == SMG_OK; lo += kSlotChunk) {
+    const uint64_t hi = std::min<uint64_t>(g->slots, lo + kSlotChunk);
+    const uint64_t ns = hi - lo;
+    cudaError_t e = cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st);
+    if (e == cudaSuccess) {
+      enum_kernel<false><<<static_cast<unsigned>(blocks), kThreads, kDynSmem, st>>>(a, lo, hi, uval, 0, nullptr);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(uval + ns, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, uval, uoff, ns + 1, st);
+    unsigned long long chunk_total = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&chunk_total, uoff + ns, sizeof(chunk_total), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      status = fail(SMG_EIO, std::string("enumerate count pass: ") + cudaGetErrorString(e));
+      break;
+    }
+    const unsigned long long take = std::min<unsigned long long>(chunk_total, lim - total);
+    const unsigned long long room = total < cap_tuples ? cap_tuples - total : 0;
+    const unsigned long long keep = std::min(take, room);  // tuples copied to the caller
+    if (keep && out) {
+      const size_t need = keep * prog.depth * sizeof(uint32_t);
+      if (need > dout_cap) {
+        if (dout) cudaFree(dout);
+        dout = nullptr;
+        e = cudaMalloc(&dout, need);
+        dout_cap = e == cudaSuccess ? need : 0;
+      }
+      if (e == cudaSuccess) e = cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st);
+      if (e == cudaSuccess) {
+        // uoff holds the unit offsets within the chunk: write tuples < keep
+        enum_kernel<true><<<static_cast<unsigned>(blocks), kThreads, kDynSmem, st>>>(a, lo, hi, uoff, keep, dout);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out + total * prog.depth, dout, need, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) status = fail(SMG_EIO, std::string("enumerate write pass: ") + cudaGetErrorString(e));
+    }
+    total += take;
+  }
+  cudaFree(uval);
+  cudaFree(uoff);
+  cudaFree(tmp);
+  if (dout) cudaFree(dout);
+  *n_out = total;
+  return status;
 }
 
 int smg_count_range(const smg_graph* g, const smg_plan* plan, int replica, uint32_t lo,

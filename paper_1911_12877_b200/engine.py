@@ -97,5 +97,28 @@ def count_shard(graph: Graph, plan, shard: int, num_shards: int, device: int = 0
     return _result(r, 1)
 
 
+def enumerate(graph: Graph, plan, limit: int | None = None, device: int = 0,
+              max_tuples: int = 1 << 24) -> list[tuple]:
+    """symmine.enumerate (python/module.cpp:176-181 -> enumerate_instances,
+    engine.cpp:181-191): embeddings as vertex tuples in the reference's order
+    (level-0 ascending, then lexicographic), truncated at `limit`."""
+    import numpy as np
+    p = _plan(plan)
+    lib = N.gpu_lib()
+    h = graph.device_handle((device,))
+    sp = p.to_smg()
+    cap = max_tuples if limit is None else min(limit, max_tuples)
+    out = np.zeros(max(cap, 1) * sp.depth, dtype=np.uint32)
+    n_out = ctypes.c_uint64()
+    N.check_gpu(lib.smg_enumerate(h, ctypes.byref(sp), 0, limit is not None,
+                                  0 if limit is None else limit,
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), cap,
+                                  ctypes.byref(n_out)))
+    if n_out.value > cap:
+        raise N.InputError(f"{n_out.value} embeddings exceed max_tuples={max_tuples}")
+    rows = out[: n_out.value * sp.depth].reshape(-1, sp.depth)
+    return [tuple(int(x) for x in r) for r in rows]
+
+
 def device_count() -> int:
     return int(N.gpu_lib().smg_device_count())

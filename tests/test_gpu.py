@@ -184,6 +184,29 @@ def test_big_config_reference_roots(cfg):
         assert got == rec["counts"], (cfg, label)
 
 
+def test_enumerate_matches_reference(golden, corpus_graphs):
+    """f4: enumerate_instances order and truncation (golden from the reference)."""
+    from paper_1911_12877_b200 import enumerate as enumerate_gpu
+    for rec in golden["enumerate"]:
+        g = corpus_graphs[rec["graph"]]
+        p = Plan.from_json(golden["plans"][rec["plan"]])
+        got = enumerate_gpu(g, p, rec["limit"])
+        assert [list(t) for t in got] == rec["tuples"], (rec["graph"], rec["plan"], rec["limit"])
+
+
+def test_enumerate_mid_size_vs_oracle(port):
+    from paper_1911_12877_b200 import enumerate as enumerate_gpu
+    g = configs.load(configs.GraphSpec("rmat", (11, 8, 0.57, 0.19, 0.19), 21))
+    for name, limit in (("triangle", None), ("rectangle", 5000), ("house", 777), ("clique:4", None),
+                        ("pentagon", 1), ("path:4", 2500)):
+        p = named_plan(name)
+        want = port.enumerate(g.offsets, g.adjacency, p.to_smg(), limit, cap=1 << 21)
+        got = enumerate_gpu(g, p, limit)
+        assert got == want, name
+        if limit is None:
+            assert len(got) == count(g, p)
+
+
 def _digest(off, adj):
     import hashlib
     h = hashlib.sha256()
