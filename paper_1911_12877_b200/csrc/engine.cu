@@ -80,6 +80,8 @@ struct KernelArgs {
   uint32_t* scratch;
   uint64_t cap;                   // scratch elements per slot
   uint64_t unit_begin, unit_end;  // edge-slot range
+  uint64_t nverts;
+  uint32_t tune;  // SMG_TUNE bits (experiments): 1 = degree-only side choice
   uint32_t shard, num_shards;
   Counters* ctr;
   uint32_t* heavy_items;          // CTA-tier queue (kHeavyItemWords per item), may be null
@@ -151,6 +153,8 @@ struct Ctx {
   uint64_t cap;
   uint32_t* hash;
   int lane;
+  float nv;  // number of vertices (id range), for window-fraction estimates
+  uint32_t tune;
 };
 
 __device__ __forceinline__ void nbrs(const Ctx& c, uint32_t v, const uint32_t*& p, uint32_t& len) {
@@ -664,6 +668,23 @@ __device__ uint64_t diff_terms(const Ctx& c, const Program& P, const BatchSets& 
   return (add_product ? static_cast<uint64_t>(b.nA) * b.nB : 0ull) - hits;
 }
 
+// Which side to stream: only the part of each streamed list inside the other
+// set's value window is read, so weigh each side's degree sum by the width of
+// the window it is clipped to (ids are unordered w.r.t. degree, so a list
+// spreads roughly uniformly over the id range).
+// Each streamed list also pays a fixed setup (offsets, window search, a
+// warp-serial pass for long lists), ~kListCost elements' worth.
+constexpr float kListCost = 48.f;
+__device__ __forceinline__ bool stream_b_cheaper(const Ctx& c, const BatchSets& b, uint64_t deg_a,
+                                                 uint64_t deg_b) {
+  if (c.tune & 1u) return deg_b < deg_a;
+  const float wa = fminf(1.f, (static_cast<float>(b.A[b.nA - 1] - b.A[0]) + 1.f) / c.nv);
+  const float wb = fminf(1.f, (static_cast<float>(b.B[b.nB - 1] - b.B[0]) + 1.f) / c.nv);
+  const float cost_a = kListCost * b.nA + static_cast<float>(deg_a) * wb;  // stream A's lists
+  const float cost_b = kListCost * b.nB + static_cast<float>(deg_b) * wa;
+  return cost_b < cost_a;
+}
+
 struct HeavyQueue {
   uint32_t* items;          // kHeavyItemWords per item
   unsigned long long cap;
@@ -686,7 +707,7 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
       sum_s = 0;
     } else {
       const uint64_t da = degree_sum(c, b.A, b.nA, 0, 32), db = degree_sum(c, b.B, b.nB, 0, 32);
-      flip = db < da;
+      flip = stream_b_cheaper(c, b, da, db);
       sum_s = flip ? db : da;
     }
     ProbeSet ps;
@@ -748,6 +769,8 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) 
   c.scratch = a.scratch + gw * static_cast<uint64_t>(P.nslots) * a.cap;
   c.cap = a.cap;
   c.lane = lane;
+  c.nv = static_cast<float>(a.nverts);
+  c.tune = a.tune;
   c.hash = dyn_smem + wib * kHashSlots;
   const bool batch = P.batch;
   HeavyQueue hq;
@@ -1130,6 +1153,8 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
   c.scratch = a.heavy_scratch + static_cast<uint64_t>(blockIdx.x) * P.nslots * a.cap;
   c.cap = a.cap;
   c.lane = lane;
+  c.nv = static_cast<float>(a.nverts);
+  c.tune = a.tune;
   c.hash = table;
   uint64_t trbuf[TRACE ? kTrCount : 1];
   if (TRACE)
@@ -1166,7 +1191,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
         sa += sh.red_a[w];
         sb += sh.red_b[w];
       }
-      flip = sb < sa;
+      flip = stream_b_cheaper(c, b, sa, sb);
       __syncthreads();
     }
     const uint32_t* Parr = flip ? b.A : b.B;
@@ -1249,6 +1274,8 @@ __global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint
   c.scratch = a.scratch + gw * static_cast<uint64_t>(P.nslots + 1) * a.cap;
   c.cap = a.cap;
   c.lane = lane;
+  c.nv = static_cast<float>(a.nverts);
+  c.tune = a.tune;
   c.hash = dyn_smem + wib * kHashSlots;
   uint32_t* leafbuf = c.scratch + static_cast<uint64_t>(P.nslots) * a.cap;
   WarpState& s = states[wib];
@@ -1363,6 +1390,10 @@ __global__ void fill_src_kernel(const unsigned long long* __restrict__ off, uint
 // ------------------------------------------------------------------ host ---
 
 thread_local std::string g_last_error;
+const uint32_t g_tune = [] {
+  const char* e = std::getenv("SMG_TUNE");
+  return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+}();
 const int g_trace = [] {
   const char* e = std::getenv("SMG_TRACE");
   return (e && *e && *e != '0') ? 1 : 0;
@@ -1476,6 +1507,8 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.cap = cap;
   a.unit_begin = L.unit_begin;
   a.unit_end = L.unit_end;
+  a.nverts = g.n;
+  a.tune = g_tune;
   a.shard = L.shard;
   a.num_shards = L.num_shards;
   a.ctr = r.ctr;
@@ -1911,6 +1944,8 @@ int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has
   a.scratch = r.scratch;
   a.cap = cap;
   a.ctr = r.ctr;
+  a.nverts = g->n;
+  a.tune = g_tune;
   a.prog = prog;
   unsigned long long total = 0;
   int status = SMG_OK;
