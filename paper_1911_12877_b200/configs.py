@@ -47,6 +47,19 @@ SPECS = {
 }
 
 
+DESCRIPTIONS = {
+    "cfg1": "ER n=65,536 m=1,048,576, triangle (v0>v1>v2)",
+    "cfg2": "RMAT scale 20 ef 16 (0.57,0.19,0.19,0.05) ids permuted, 4-clique + induced 4-cycle",
+    "cfg3": "Chung-Lu n=4M m=43M gamma 2.1 w_max 20,000, 5-clique + house",
+    "cfg4": "RMAT scale 22 ef 16, all six connected 4-vertex motifs (motif-mode plans)",
+    "cfg5": "Chung-Lu n=3M m=117M gamma 2.3 w_max 30,000, induced 5-cycle + tailed diamond (both readings)",
+}
+
+
+def describe(cfg: str) -> str:
+    return DESCRIPTIONS[cfg]
+
+
 def config_patterns(cfg: str) -> list[tuple[str, Plan]]:
     """(label, plan) pairs counted on each config."""
     if cfg == "cfg1":

@@ -70,7 +70,8 @@ struct Counters {
 enum {
   kTrUnits = 0, kTrBuildCycles, kTrBatchCycles, kTrBatches, kTrBatchesHashed, kTrStreamElems,
   kTrSearchLists, kTrProbeSetSum, kTrStreamSetSum, kTrLeafCycles, kTrLeaves, kTrBigPCycles,
-  kTrDeferred, kTrHeavyItems, kTrHeavyCycles, kTrLongLists, kTrHeavyBuild, kTrHeavyStream, kTrCount
+  kTrDeferred, kTrHeavyItems, kTrHeavyCycles, kTrLongLists, kTrHeavyBuild, kTrHeavyStream,
+  kTrWarpBusySum, kTrWarpBusyMax, kTrCount
 };
 
 struct KernelArgs {
@@ -81,12 +82,14 @@ struct KernelArgs {
   uint64_t cap;                   // scratch elements per slot
   uint64_t unit_begin, unit_end;  // edge-slot range
   uint64_t nverts;
-  uint32_t tune;  // SMG_TUNE bits (experiments): 1 = degree-only side choice
+  uint32_t tune;  // SMG_TUNE bits (experiments): 1 = degree-only side choice, 2 = no clique-local
   uint32_t shard, num_shards;
   Counters* ctr;
   uint32_t* heavy_items;          // CTA-tier queue (kHeavyItemWords per item), may be null
   unsigned long long heavy_cap;
   uint32_t* heavy_scratch;        // CTA-tier node scratch (nslots * cap per CTA)
+  uint32_t* local_rows;           // clique-local rows, warp tier (per warp), or null
+  uint32_t* heavy_rows;           // clique-local rows, CTA tier (per CTA)
   Program prog;
 };
 
@@ -691,6 +694,7 @@ struct HeavyQueue {
   unsigned long long* count;
 };
 constexpr int kHeavyItemWords = 6;  // v_0 .. v_{n-3}, n <= 8
+constexpr uint32_t kCliqueItem = 0xffffffffu;  // last word of a clique-local item (never an id)
 
 // Warp tier.  Returns the batch total, or defers it to the heavy queue.
 template <bool TRACE>
@@ -727,6 +731,7 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
         slot = __shfl_sync(kFull, slot, 0);
         if (slot < hq.cap) {
           if (c.lane < P.depth - 2) hq.items[slot * kHeavyItemWords + c.lane] = s.vals[c.lane];
+          else if (c.lane == kHeavyItemWords - 1) hq.items[slot * kHeavyItemWords + c.lane] = 0u;
           if (TRACE) tr[kTrDeferred] += 1;
           return 0;
         }
@@ -752,6 +757,247 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
   }
   if (!P.batch_diff) return core;
   return diff_terms(c, P, b, 0, 32, true) - core;
+}
+
+// ------------------------------------------------------------ clique-local ---
+// Clique plans (no difference sources): every level >= 2 is a subset of
+// U = N(v0) & N(v1).  Per unit the induced subgraph on U is built once as
+// bitmap rows over U's local ids (local id = rank in sorted U, so value order
+// = id order and every bound becomes a bit prefix), then the nested loops of
+// levels 2..n-1 run as word-wise ANDs with a popcount leaf.  The reference
+// re-merges full neighbour lists at every level of every prefix
+// (engine.cpp:58-80); here each neighbour list is read once per unit.
+// Warp tier: |U| <= kLocalWarpMax (one row word per lane); bigger units go to
+// the CTA tier (heavy_kernel) with |U| <= kLocalCtaMax; beyond that the
+// generic path runs.
+
+constexpr uint32_t kLocalWarpMax = 512;
+constexpr uint32_t kLocalCtaMax = 4096;
+constexpr uint32_t kLocalCtaSlots = 2 * kLocalCtaMax;            // index table slots
+constexpr uint32_t kLocalRowWords = kLocalCtaMax / 32;           // CTA row stride (words)
+constexpr uint32_t kLocalWarpRowWords = kLocalWarpMax / 32;      // warp row stride (words)
+constexpr size_t kHeavyCliqueSmem = kLocalCtaSlots * 4 + kLocalCtaSlots * 2 +
+                                    kHeavyWarps * kLocalRowWords * 4;
+constexpr uint16_t kNoIdx = 0xFFFF;
+
+struct LocalIndex {
+  uint32_t* keys;   // bucketised like the probe tables
+  uint16_t* idx;    // local id of the key in the same slot
+  int bits;
+};
+
+// Build the value -> local id table for U[0..u) with threads [tid, tid+nth).
+__device__ void local_index_build(LocalIndex& L, const uint32_t* U, uint32_t u, int tid, int nth,
+                                  bool cta) {
+  int bits = 6;
+  while ((1u << bits) < 2 * u) ++bits;
+  L.bits = bits;
+  const uint32_t nb = 1u << (bits - 2);
+  uint4* kb = reinterpret_cast<uint4*>(L.keys);
+  if (cta) __syncthreads(); else __syncwarp();
+  for (uint32_t i = tid; i < nb; i += nth) kb[i] = make_uint4(kEmptySlot, kEmptySlot, kEmptySlot, kEmptySlot);
+  if (cta) __syncthreads(); else __syncwarp();
+  const uint32_t mask = nb - 1u;
+  for (uint32_t i = tid; i < u; i += nth) {
+    const uint32_t key = U[i];
+    uint32_t h = hbucket(key, bits - 2);
+    for (;;) {
+      uint32_t* bk = L.keys + 4 * h;
+      int j = -1;
+      if (atomicCAS(bk, kEmptySlot, key) == kEmptySlot) j = 0;
+      else if (atomicCAS(bk + 1, kEmptySlot, key) == kEmptySlot) j = 1;
+      else if (atomicCAS(bk + 2, kEmptySlot, key) == kEmptySlot) j = 2;
+      else if (atomicCAS(bk + 3, kEmptySlot, key) == kEmptySlot) j = 3;
+      if (j >= 0) {
+        L.idx[4 * h + j] = static_cast<uint16_t>(i);
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+  if (cta) __syncthreads(); else __syncwarp();
+}
+
+__device__ __forceinline__ int local_find(const LocalIndex& L, uint32_t y) {
+  const int bbits = L.bits - 2;
+  const uint32_t mask = (1u << bbits) - 1u;
+  const uint4* kb = reinterpret_cast<const uint4*>(L.keys);
+  uint32_t h = hbucket(y, bbits);
+  for (;;) {
+    const uint4 q = kb[h];
+    if (q.x == y) return L.idx[4 * h];
+    if (q.y == y) return L.idx[4 * h + 1];
+    if (q.z == y) return L.idx[4 * h + 2];
+    if (q.w == y) return L.idx[4 * h + 3];
+    if (q.w == kEmptySlot) return -1;
+    h = (h + 1) & mask;
+  }
+}
+
+// Row a of the local graph: bits of N(U[a]) & U restricted to values in
+// [U[0], hi) into rowbuf (nwords words, zeroed by the caller), then stored to
+// row (coalesced).  One warp per row.
+__device__ void local_row(const Ctx& c, const LocalIndex& L, const uint32_t* U, uint32_t u,
+                          uint32_t a, bool lower_only, uint32_t* rowbuf, uint32_t nwords,
+                          uint32_t* row) {
+  const uint32_t x = U[a];
+  const uint32_t lo = U[0];
+  const uint32_t hi = lower_only ? x : U[u - 1] + 1u;
+  const uint32_t* p;
+  uint32_t deg;
+  nbrs(c, x, p, deg);
+  uint32_t start = 0;
+  if (deg && lo < hi) {
+    const uint32_t first = __ldg(p);
+    if (first < lo) start = lower_bound_dev(p, deg, lo);
+    for (uint32_t t0 = start; t0 < deg; t0 += 32 * kUnroll) {
+      uint32_t y[kUnroll];
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) {
+        const uint32_t i = t0 + k * 32 + c.lane;
+        y[k] = i < deg ? __ldg(p + i) : kEmptySlot;
+      }
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) {
+        if (y[k] < hi) {
+          const int id = local_find(L, y[k]);
+          if (id >= 0) atomicOr(&rowbuf[id >> 5], 1u << (id & 31));
+        }
+      }
+      if (__any_sync(kFull, y[kUnroll - 1] >= hi)) break;
+    }
+  }
+  __syncwarp();
+  for (uint32_t w = c.lane; w < nwords; w += 32) {
+    row[w] = rowbuf[w];
+    rowbuf[w] = 0u;
+  }
+  __syncwarp();
+}
+
+// First set bit (ascending) of the WPL*32-word bitmap held as rem[k] in lane
+// `lane` (word index k*32 + lane); clears it and returns its bit index, or -1.
+template <int WPL>
+__device__ __forceinline__ int local_pop_next(uint32_t (&rem)[WPL], int lane) {
+#pragma unroll
+  for (int k = 0; k < WPL; ++k) {
+    const unsigned nz = __ballot_sync(kFull, rem[k] != 0u);
+    if (nz) {
+      const int f = __ffs(nz) - 1;
+      const uint32_t w = __shfl_sync(kFull, rem[k], f);
+      const int bit = __ffs(w) - 1;
+      if (lane == f) rem[k] &= rem[k] - 1u;
+      return (k * 32 + f) * 32 + bit;
+    }
+  }
+  return -1;
+}
+
+template <int WPL>
+__device__ __forceinline__ void prefix_mask(uint32_t q, int lane, uint32_t (&m)[WPL]) {
+#pragma unroll
+  for (int k = 0; k < WPL; ++k) {
+    const uint32_t w0 = (k * 32 + lane) * 32u;
+    m[k] = q >= w0 + 32u ? ~0u : (q <= w0 ? 0u : ((1u << (q - w0)) - 1u));
+  }
+}
+
+// Levels 2..n-1 on the local graph (rows of `stride` words).  Level-2 ids
+// are taken when (ordinal % a2_stride) == a2_first, so CTA warps can share a
+// unit.  Returns this warp's count (all lanes hold it).
+template <int WPL>
+__device__ uint64_t local_dfs(const Ctx& c, const Program& P, const uint32_t* rows, uint32_t stride,
+                              uint32_t u, uint32_t q0, uint32_t q1, uint32_t a2_first,
+                              uint32_t a2_stride) {
+  const int n = P.depth;
+  const int lane = c.lane;
+  uint32_t acc[kMaxLevels][WPL];
+  uint32_t rem[kMaxLevels][WPL];
+  int a[kMaxLevels];
+  auto bound_q = [&](int i) -> uint32_t {
+    const int p = P.parent[i];
+    return p < 0 ? u : (p == 0 ? q0 : (p == 1 ? q1 : static_cast<uint32_t>(a[p])));
+  };
+  uint32_t m[WPL];
+  prefix_mask<WPL>(bound_q(2), lane, m);
+#pragma unroll
+  for (int k = 0; k < WPL; ++k) rem[2][k] = m[k];
+  uint64_t total = 0;
+  uint32_t ord2 = 0;
+  int level = 2;
+  while (level >= 2) {
+    const int x = local_pop_next<WPL>(rem[level], lane);
+    if (x < 0) {
+      --level;
+      continue;
+    }
+    if (level == 2 && (ord2++ % a2_stride) != a2_first) continue;
+    a[level] = x;
+    const uint32_t* row = rows + static_cast<uint64_t>(x) * stride;
+    uint32_t nacc[WPL];
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+      const uint32_t w = k * 32 + lane;
+      const uint32_t r = w < stride ? row[w] : 0u;
+      nacc[k] = level == 2 ? r : (acc[level][k] & r);
+    }
+    if (level + 1 == n - 1) {
+      prefix_mask<WPL>(bound_q(n - 1), lane, m);
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int k = 0; k < WPL; ++k) cnt += __popc(nacc[k] & m[k]);
+      total += cnt;
+    } else {
+      ++level;
+      prefix_mask<WPL>(bound_q(level), lane, m);
+#pragma unroll
+      for (int k = 0; k < WPL; ++k) {
+        acc[level][k] = nacc[k];
+        rem[level][k] = nacc[k] & m[k];
+      }
+    }
+  }
+  return warp_sum64(total);
+}
+
+// The universe U: the longest stored k=1 node (all are N(v0) & N(v1) bounded).
+__device__ __forceinline__ int clique_universe(const WarpState& s, const Program& P) {
+  int best = -1;
+  for (int t = P.node_begin[1]; t < P.node_end[1]; ++t)
+    if (best < 0 || s.len[t] > s.len[best]) best = t;
+  return best;
+}
+
+// Rows only need bits below their own id when every deeper level is bounded
+// by the level before it (the standard clique restrictions v_i < v_{i-1}).
+__device__ __forceinline__ bool clique_lower_only(const Program& P) {
+  for (int i = 3; i < P.depth; ++i)
+    if (P.parent[i] != i - 1) return false;
+  return true;
+}
+
+// Warp tier: count the unit in the warp's state (k=1 nodes built).
+__device__ uint64_t clique_local_warp(const Ctx& c, const Program& P, uint32_t* rows) {
+  const WarpState& s = *c.s;
+  const int un = clique_universe(s, P);
+  const uint32_t* U = s.ptr[un];
+  const uint32_t u = s.len[un];
+  if (u < 2) return 0;  // levels 2..n-1 need n-2 >= 3 distinct elements of U
+  LocalIndex L;
+  L.keys = c.hash;
+  L.idx = reinterpret_cast<uint16_t*>(c.hash + 2 * kLocalWarpMax);
+  uint32_t* rowbuf = c.hash + 2 * kLocalWarpMax + kLocalWarpMax;  // after keys (2u) and idx (u/2 words)
+  local_index_build(L, U, u, c.lane, 32, false);
+  const uint32_t nwords = (u + 31) / 32;
+  if (c.lane < kLocalWarpRowWords) rowbuf[c.lane] = 0u;
+  __syncwarp();
+  const bool lower = clique_lower_only(P);
+  for (uint32_t a = 0; a < u; ++a)
+    local_row(c, L, U, u, a, lower, rowbuf, nwords, rows + static_cast<uint64_t>(a) * kLocalWarpRowWords);
+  __syncwarp();
+  const uint32_t q0 = lower_bound_rw(U, u, s.vals[0]);
+  const uint32_t q1 = lower_bound_rw(U, u, s.vals[1]);
+  return local_dfs<1>(c, P, rows, kLocalWarpRowWords, u, q0, q1, 0, 1);
 }
 
 template <bool METER, bool TRACE>
@@ -782,6 +1028,8 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) 
     for (int i = 0; i < kTrCount; ++i) trbuf[i] = 0;
   uint64_t* tr = trbuf;
   long long tclk = 0;
+  unsigned long long t_start = 0;
+  if (TRACE) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   WarpState& s = states[wib];
 
   uint64_t cnt = 0, elems = 0, units = 0;
@@ -824,6 +1072,24 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) 
       if (P.depth == 3) {
         checked_acc(cnt, leaf_count(c, P), ovf);
         continue;
+      }
+      if (!METER && P.clique && a.local_rows && !(a.tune & 2u)) {
+        const uint32_t u = s.len[clique_universe(s, P)];
+        if (u <= kLocalWarpMax) {
+          checked_acc(cnt, clique_local_warp(c, P, a.local_rows + gw * kLocalWarpMax * kLocalWarpRowWords),
+                      ovf);
+          continue;
+        }
+        if (u <= kLocalCtaMax && hq.items) {  // CTA tier
+          unsigned long long slot = 0;
+          if (lane == 0) slot = atomicAdd(hq.count, 1ull);
+          slot = __shfl_sync(kFull, slot, 0);
+          if (slot < hq.cap) {
+            if (lane < 2) hq.items[slot * kHeavyItemWords + lane] = s.vals[lane];
+            if (lane == kHeavyItemWords - 1) hq.items[slot * kHeavyItemWords + lane] = kCliqueItem;
+            continue;
+          }
+        }
       }
       if (batch && P.depth == 4) {
         if (METER) elems += meter_batch(c, P);
@@ -878,6 +1144,11 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) 
     if (ovf) atomicOr(&a.ctr->overflow, 1u);
     if (TRACE) {
       tr[kTrUnits] = units;
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      const unsigned long long busy = now - t_start;
+      tr[kTrWarpBusySum] = busy;
+      atomicMax(&a.ctr->trace[kTrWarpBusyMax], busy);
       for (int i = 0; i < kTrCount; ++i)
         if (tr[i]) atomicAdd(&a.ctr->trace[i], static_cast<unsigned long long>(tr[i]));
     }
@@ -1171,7 +1442,46 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
     if (it >= nitems) break;
     long long t0 = TRACE ? clock64() : 0;
     if (threadIdx.x < P.depth - 2) sh.st.vals[threadIdx.x] = a.heavy_items[it * kHeavyItemWords + threadIdx.x];
+    const bool clique_item = a.heavy_items[it * kHeavyItemWords + kHeavyItemWords - 1] == kCliqueItem;
     __syncthreads();
+    if (clique_item) {
+      // CTA clique-local: k=0,1 nodes, U, index table, rows by all warps, split DFS
+      for (int t = P.node_begin[0]; t < P.node_end[1]; ++t) cta_build_node(c, P, t, sh, table);
+      const int un = clique_universe(sh.st, P);
+      const uint32_t* U = sh.st.ptr[un];
+      const uint32_t u = sh.st.len[un];
+      LocalIndex L;
+      L.keys = table;
+      L.idx = reinterpret_cast<uint16_t*>(table + kLocalCtaSlots);
+      uint32_t* rowbuf = table + kLocalCtaSlots + kLocalCtaSlots / 2 + warp * kLocalRowWords;
+      local_index_build(L, U, u, threadIdx.x, kHeavyThreads, true);
+      for (uint32_t w = lane; w < kLocalRowWords; w += 32) rowbuf[w] = 0u;
+      __syncwarp();
+      const uint32_t nwords = (u + 31) / 32;
+      const bool lower = clique_lower_only(P);
+      uint32_t* rows = a.heavy_rows + static_cast<uint64_t>(blockIdx.x) * kLocalCtaMax * kLocalRowWords;
+      for (uint32_t r = warp; r < u; r += kHeavyWarps)
+        local_row(c, L, U, u, r, lower, rowbuf, nwords, rows + static_cast<uint64_t>(r) * kLocalRowWords);
+      __threadfence_block();
+      __syncthreads();
+      const uint32_t q0 = lower_bound_rw(U, u, sh.st.vals[0]);
+      const uint32_t q1 = lower_bound_rw(U, u, sh.st.vals[1]);
+      const uint64_t part = local_dfs<kLocalRowWords / 32>(c, P, rows, kLocalRowWords, u, q0, q1, warp,
+                                                          kHeavyWarps);
+      if (lane == 0) sh.red_a[warp] = part;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint64_t sum = 0;
+        for (int w = 0; w < kHeavyWarps; ++w) sum += sh.red_a[w];
+        checked_acc(cnt, sum, ovf);
+        if (TRACE) {
+          tr[kTrHeavyItems] += 1;
+          tr[kTrHeavyCycles] += clock64() - t0;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     for (int t = P.node_begin[0]; t < P.node_end[P.depth - 3]; ++t) cta_build_node(c, P, t, sh, table);
     long long t1 = TRACE ? clock64() : 0;
     if (TRACE && threadIdx.x == 0) tr[kTrHeavyBuild] += t1 - t0;
@@ -1421,6 +1731,10 @@ struct Replica {
   size_t scratch_bytes = 0;
   uint32_t* heavy_items = nullptr;     // CTA-tier queue
   uint32_t* heavy_scratch = nullptr;
+  uint32_t* local_rows = nullptr;      // clique-local rows (warp tier)
+  size_t local_rows_bytes = 0;
+  uint32_t* heavy_rows = nullptr;      // clique-local rows (CTA tier)
+  size_t heavy_rows_bytes = 0;
   size_t heavy_scratch_bytes = 0;
   Counters* ctr = nullptr;  // device
   Counters* host_ctr = nullptr;  // pinned
@@ -1491,6 +1805,25 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
       r.heavy_scratch_bytes = hs;
     }
   }
+  const bool clique = !METER && prog.clique;
+  if (clique) {
+    const size_t lr = blocks * kWarpsPerBlock * kLocalWarpMax * kLocalWarpRowWords * sizeof(uint32_t);
+    const size_t hr = static_cast<size_t>(r.num_sms) * 4 * kLocalCtaMax * kLocalRowWords * sizeof(uint32_t);
+    if (r.local_rows_bytes < lr) {
+      if (r.local_rows) cudaFree(r.local_rows);
+      r.local_rows = nullptr;
+      r.local_rows_bytes = 0;
+      SMG_CUDA(cudaMalloc(&r.local_rows, lr));
+      r.local_rows_bytes = lr;
+    }
+    if (r.heavy_rows_bytes < hr) {
+      if (r.heavy_rows) cudaFree(r.heavy_rows);
+      r.heavy_rows = nullptr;
+      r.heavy_rows_bytes = 0;
+      SMG_CUDA(cudaMalloc(&r.heavy_rows, hr));
+      r.heavy_rows_bytes = hr;
+    }
+  }
   cudaStream_t st = r.active();
   SMG_CUDA(cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st));
   SMG_CUDA(cudaEventRecord(r.ev0, st));
@@ -1515,17 +1848,19 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.heavy_items = heavy ? r.heavy_items : nullptr;
   a.heavy_cap = heavy ? kHeavyQueueCap : 0;
   a.heavy_scratch = r.heavy_scratch;
+  a.local_rows = clique ? r.local_rows : nullptr;
+  a.heavy_rows = clique ? r.heavy_rows : nullptr;
   a.prog = prog;
   if (L.unit_end > L.unit_begin) {
     count_kernel<METER, TRACE><<<static_cast<unsigned>(blocks), kThreads, kDynSmem, st>>>(a);
     if (heavy) {
+      const size_t hsm = clique ? std::max(kHeavySmem, kHeavyCliqueSmem) : kHeavySmem;
       SMG_CUDA(cudaFuncSetAttribute(heavy_kernel<TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kHeavySmem)));
+                                    static_cast<int>(hsm)));
       int hper = 0;
-      SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hper, heavy_kernel<TRACE>, kHeavyThreads,
-                                                             kHeavySmem));
-      hper = std::max(1, hper);
-      heavy_kernel<TRACE><<<r.num_sms * hper, kHeavyThreads, kHeavySmem, st>>>(a);
+      SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hper, heavy_kernel<TRACE>, kHeavyThreads, hsm));
+      hper = std::min(4, std::max(1, hper));
+      heavy_kernel<TRACE><<<r.num_sms * hper, kHeavyThreads, hsm, st>>>(a);
     }
   }
   SMG_CUDA(cudaGetLastError());
@@ -1556,7 +1891,8 @@ int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* 
                                           "probe_set_sum", "stream_set_sum", "leaf_cycles",
                                           "leaves", "bigP_stream_cycles", "deferred",
                                           "heavy_items", "heavy_cycles", "long_lists",
-                                          "heavy_build_cycles", "heavy_stream_cycles"};
+                                          "heavy_build_cycles", "heavy_stream_cycles",
+                                          "warp_busy_sum_ns", "warp_busy_max_ns"};
     std::fprintf(stderr, "[smg trace] kernel %.3f ms:", t);
     for (int i = 0; i < kTrCount; ++i)
       std::fprintf(stderr, " %s=%.4g", names[i], static_cast<double>(r.host_ctr->trace[i]));
@@ -1627,7 +1963,10 @@ int smg_plan_describe(const smg_plan* plan, char* buf, size_t cap) {
   s += "],\"leaf\":" + (pr.depth >= 3 ? node_json(pr.leaf) : std::string("null"));
   s += ",\"batch\":" + std::to_string(pr.batch) + ",\"batch_diff\":" + std::to_string(pr.batch_diff) +
        ",\"batch_yltx\":" + std::to_string(pr.batch_yltx) +
-       ",\"batch_fixed_bound\":" + std::to_string(pr.batch_fixed_bound) + "}";
+       ",\"batch_fixed_bound\":" + std::to_string(pr.batch_fixed_bound) +
+       ",\"clique\":" + std::to_string(pr.clique) + ",\"parent\":[";
+  for (int i = 0; i < pr.depth; ++i) s += (i ? "," : "") + std::to_string(pr.parent[i]);
+  s += "]}";
   if (s.size() + 1 > cap) return fail(SMG_EINPUT, "buffer too small");
   std::memcpy(buf, s.c_str(), s.size() + 1);
   return SMG_OK;
@@ -1643,6 +1982,8 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->scratch) cudaFree(r->scratch);
     if (r->heavy_items) cudaFree(r->heavy_items);
     if (r->heavy_scratch) cudaFree(r->heavy_scratch);
+    if (r->local_rows) cudaFree(r->local_rows);
+    if (r->heavy_rows) cudaFree(r->heavy_rows);
     if (r->ctr) cudaFree(r->ctr);
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
     if (r->ev0) cudaEventDestroy(r->ev0);

@@ -76,7 +76,11 @@ struct Program {
   int8_t batch_diff;              // leaf op is -N[x] (else & N(x))
   int8_t batch_yltx;              // leaf bound is x itself (y < x)
   int8_t batch_fixed_bound;       // leaf bound level < n-2 (fixed over siblings), -1 none
-  int8_t pad[3];
+  // Clique plans (every source an intersection, depth >= 5): every level >= 2
+  // lives inside U = N(v0) & N(v1), so a unit is counted on the local graph
+  // of U as bitmaps (engine.cu, clique-local).
+  int8_t clique;
+  int8_t pad[2];
   Node leaf;                      // C_{depth-1}, counted not stored (depth >= 3)
   Node nodes[kMaxNodes];
 };
@@ -201,6 +205,9 @@ inline std::string compile_program(const smg_plan& p, Program* out) {
   pr.nnodes = nt;
   pr.nslots = slots;
   pr.batch_fixed_bound = -1;
+  pr.clique = n >= 5 ? 1 : 0;
+  for (int i = 1; i < n; ++i)
+    if (p.diff_mask[i]) pr.clique = 0;
   if (n >= 4 && pr.leaf.src >= 0 && pr.leaf.nops == 1 && pr.leaf.ops[0].level == n - 2) {
     pr.batch = 1;
     pr.batch_diff = pr.leaf.ops[0].mode == kOpDiff ? 1 : 0;

@@ -221,6 +221,74 @@ def test_program_interpreter_matches_reference_golden(golden, port):
     assert checked > 1500
 
 
+def clique_local_model(prog, off, adj):
+    """engine.cu clique-local: per unit, bitmap rows over U = the longest k=1
+    node (sorted, local id = rank), then levels 2..n-1 as prefix-masked ANDs."""
+    n = len(off) - 1
+    lists = [adj[off[v]:off[v + 1]].tolist() for v in range(n)]
+    nb = [set(x) for x in lists]
+    depth = prog["depth"]
+    parent = prog["parent"]
+    lower = all(parent[i] == i - 1 for i in range(3, depth))
+    total = 0
+    for v0 in range(n):
+        for v1 in lists[v0]:
+            if prog["unit_bound"] and not v1 < v0:
+                continue
+            vals = [v0, v1]
+            best = None
+            for t in range(prog["node_begin"][1], prog["node_end"][1]):
+                nd = prog["nodes"][t]
+                u = sorted(nb[v0] & nb[v1])
+                if nd["bound"] >= 0:
+                    u = [x for x in u if x < vals[nd["bound"]]]
+                if best is None or len(u) > len(best):
+                    best = u
+            U = best
+            rows = [{b for b, y in enumerate(U) if y in nb[x] and (not lower or y < x)} for x in U]
+            q = {0: sum(1 for x in U if x < v0), 1: sum(1 for x in U if x < v1)}
+
+            def bound(i, a):
+                p = parent[i]
+                return len(U) if p < 0 else (q[p] if p < 2 else a[p])
+
+            def dfs(level, acc, a):
+                nonlocal total
+                cand = [b for b in acc if b < bound(level, a)]
+                if level == depth - 1:
+                    total += len(cand)
+                    return
+                for b in sorted(cand):
+                    a2 = dict(a)
+                    a2[level] = b
+                    dfs(level + 1, (acc & rows[b]), a2)
+
+            dfs(2, set(range(len(U))), {})
+    return total
+
+
+def test_clique_local_model_matches_reference(golden, port):
+    """The clique-local evaluation (bitmap rows, prefix masks, lower-triangular
+    rows only under the standard chain) equals the reference on the corpus."""
+    graphs = {k: port.from_edges(v["n"], v["edges"]) for k, v in golden["graphs"].items()}
+    n_checked = 0
+    for rec in golden["counts"]:
+        if not rec["plan"].startswith("clique:") or int(rec["plan"].split(":")[1]) < 5:
+            continue
+        g = golden["graphs"][rec["graph"]]
+        if g["n"] > 15 and not rec["use_restrictions"]:
+            continue
+        p = Plan.from_json(golden["plans"][rec["plan"]])
+        p = p.with_options(rec["use_restrictions"], rec["use_bounds"]) if rec["use_restrictions"] \
+            else p.with_options(False, rec["use_bounds"])
+        prog = describe(p)
+        assert prog["clique"] == 1
+        off, adj, _, _ = graphs[rec["graph"]]
+        assert clique_local_model(prog, off, adj) == rec["count"], rec
+        n_checked += 1
+    assert n_checked > 20
+
+
 def test_batchable_plans():
     for name, k in (("clique", 4), ("rectangle", 0), ("house", 0), ("pentagon", 0), ("clique", 5)):
         assert describe(named_plan(name, k))["batch"] == 1, name
