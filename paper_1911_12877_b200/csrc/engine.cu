@@ -42,14 +42,18 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kHashLog2 = 11;  // per-warp shared-memory hash: 2048 slots (8 KB)
 constexpr uint32_t kHashSlots = 1u << kHashLog2;
 constexpr uint32_t kEmptySlot = 0xffffffffu;  // never a vertex id (ids < n < 2^32)
-constexpr size_t kDynSmem = sizeof(uint32_t) * kHashSlots * kWarpsPerBlock;
-// CTA tier (heavy_kernel): 16 warps share one 16K-slot (64 KB) table.
-constexpr int kHeavyWarps = 8;
+constexpr uint32_t kDescWords = 168;  // excl[33] lo[32] hi[32] ptr[32] (8-byte aligned)
+constexpr size_t kDynSmem = sizeof(uint32_t) * (kHashSlots + kDescWords) * kWarpsPerBlock;
+// CTA tier (heavy_kernel): one 32-warp CTA per SM.  Node builds probe a
+// 8K-slot (32 KB) hash table; the batched leaf probes a 1M-bit (128 KB)
+// bitmap of the probe set over an id slice.
+constexpr int kHeavyWarps = 32;
 constexpr int kHeavyThreads = kHeavyWarps * 32;
-constexpr uint32_t kHeavySlots = 1u << 13;  // 32 KB: four CTAs per SM overlap their phases
-constexpr uint32_t kHeavyChunk = kHeavySlots / 2;  // probe-set elements per table fill
-constexpr size_t kHeavySmem = sizeof(uint32_t) * kHeavySlots;
-constexpr uint64_t kHeavyMinStream = 4096;  // defer only batches with real streaming work
+constexpr uint32_t kHeavySlots = 1u << 13;
+constexpr uint32_t kBitmapWords = 1u << 15;                 // 128 KB
+constexpr uint64_t kBitmapSpan = uint64_t(kBitmapWords) * 32;  // ids per slice
+constexpr size_t kHeavySmem = sizeof(uint32_t) * (kHeavySlots + kBitmapWords);
+constexpr uint64_t kHeavyMinStream = 32768;  // defer only batches with real streaming work
 constexpr uint64_t kHeavyQueueCap = 1ull << 24;
 
 // ---------------------------------------------------------------- device ---
@@ -71,7 +75,7 @@ enum {
   kTrUnits = 0, kTrBuildCycles, kTrBatchCycles, kTrBatches, kTrBatchesHashed, kTrStreamElems,
   kTrSearchLists, kTrProbeSetSum, kTrStreamSetSum, kTrLeafCycles, kTrLeaves, kTrBigPCycles,
   kTrDeferred, kTrHeavyItems, kTrHeavyCycles, kTrLongLists, kTrHeavyBuild, kTrHeavyStream,
-  kTrWarpBusySum, kTrWarpBusyMax, kTrCount
+  kTrWarpBusySum, kTrWarpBusyMax, kTrHeavyElems, kTrHeavyTiles, kTrCount
 };
 
 struct KernelArgs {
@@ -83,6 +87,8 @@ struct KernelArgs {
   uint64_t unit_begin, unit_end;  // edge-slot range
   uint64_t nverts;
   uint32_t tune;  // SMG_TUNE bits (experiments): 1 = degree-only side choice, 2 = no clique-local
+  uint32_t heavy_stream;  // SMG_HEAVY_STREAM: CTA-tier threshold on a batch's streamed elements
+  uint32_t heavy_min;     // SMG_HEAVY_MIN: big-probe-set batches stream at least this to be deferred
   uint32_t shard, num_shards;
   Counters* ctr;
   uint32_t* heavy_items;          // CTA-tier queue (kHeavyItemWords per item), may be null
@@ -158,6 +164,9 @@ struct Ctx {
   int lane;
   float nv;  // number of vertices (id range), for window-fraction estimates
   uint32_t tune;
+  uint32_t heavy_stream;  // defer batches streaming at least this many elements (0: off)
+  uint32_t* desc;         // per-warp list-descriptor area (kDescWords), warp tier only
+  uint32_t heavy_min;     // defer big-probe-set batches only above this streamed degree sum
 };
 
 __device__ __forceinline__ void nbrs(const Ctx& c, uint32_t v, const uint32_t*& p, uint32_t& len) {
@@ -183,6 +192,8 @@ struct ProbeSet {
   uint32_t lo, hi;      // arr[0], arr[n-1]
   uint32_t* hash;       // shared-memory table, valid when bits > 0
   int bits;
+  const uint32_t* bm;   // CTA tier: bitmap of the set over ids [bm_base, bm_base + kBitmapSpan)
+  uint32_t bm_base;
 };
 
 // The table is bucketised: a key hashes to a bucket of 4 consecutive slots
@@ -571,6 +582,53 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
     const uint32_t tot = __shfl_sync(kFull, incl, 31);
     const uint32_t excl = incl - slen;
     if (TRACE) tr[kTrStreamElems] += tot;
+    if (c.tune & 4u) {
+      // list descriptors in shared memory; every lane expands runs of kRun
+      // consecutive elements of the concatenation (one owner search per run)
+      uint32_t* dex = c.desc;
+      uint32_t* dlo = c.desc + 40;
+      uint32_t* dhi = c.desc + 72;
+      const uint32_t** dptr = reinterpret_cast<const uint32_t**>(c.desc + 104);
+      __syncwarp();
+      dex[c.lane] = excl;
+      if (c.lane == 0) dex[32] = tot;
+      dlo[c.lane] = lo_val;
+      dhi[c.lane] = hi_val;
+      dptr[c.lane] = base - excl;
+      __syncwarp();
+      constexpr uint32_t kRun = 4;
+      for (uint32_t t0 = c.lane * kRun; t0 < tot; t0 += 32 * kRun) {
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1)
+          if (dex[j + step] <= t0) j += step;
+        const uint32_t* vp = dptr[j];
+        uint32_t lo = dlo[j], hi = dhi[j], nxt = dex[j + 1];
+        uint32_t y[kRun];
+        bool in[kRun];
+#pragma unroll
+        for (uint32_t k = 0; k < kRun; ++k) {
+          const uint32_t e = t0 + k;
+          in[k] = false;
+          y[k] = 0;
+          if (e < tot) {
+            while (nxt <= e) {
+              ++j;
+              vp = dptr[j];
+              lo = dlo[j];
+              hi = dhi[j];
+              nxt = dex[j + 1];
+            }
+            y[k] = __ldg(vp + e);
+            in[k] = y[k] >= lo && y[k] < hi;
+          }
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kRun; ++k)
+          if (in[k] && probe(P, y[k])) ++hits;
+      }
+      __syncwarp();
+    } else
     for (uint32_t t = 0; t < tot; t += 64) {
       uint32_t y[2], ylo[2], yhi[2];
 #pragma unroll
@@ -628,7 +686,15 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
 __device__ __forceinline__ uint64_t degree_sum(const Ctx& c, const uint32_t* X, uint32_t n,
                                                uint32_t first, uint32_t stride) {
   uint64_t acc = 0;
-  for (uint32_t i = first + c.lane; i < n; i += stride) {
+  uint32_t i = first + c.lane;
+  for (; i + 3 * stride < n; i += 4 * stride) {  // four lists' offsets in flight
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = X[i + k * stride];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc += __ldg(c.off + v[k] + 1) - __ldg(c.off + v[k]);
+  }
+  for (; i < n; i += stride) {
     const uint32_t v = X[i];
     acc += __ldg(c.off + v + 1) - __ldg(c.off + v);
   }
@@ -688,6 +754,37 @@ __device__ __forceinline__ bool stream_b_cheaper(const Ctx& c, const BatchSets& 
   return cost_b < cost_a;
 }
 
+// Side choice with a lazy degree sum: the smaller set's degree sum first; the
+// larger set's cost is at least kListCost + 1 window element per list, and
+// when that bound already loses its degree sum (a long, latency-bound loop
+// for hub-sized sets) is skipped.  `dsum(X, n)` returns the full degree sum
+// of X[0..n) on every participating thread.  Returns flip (= stream B) and
+// the streamed side's degree sum.
+template <class DegSum>
+__device__ __forceinline__ bool choose_stream_b(const Ctx& c, const BatchSets& b, DegSum dsum,
+                                                uint64_t& sum_s) {
+  const bool a_small = b.nA <= b.nB;
+  const uint32_t* X = a_small ? b.A : b.B;
+  const uint32_t nX = a_small ? b.nA : b.nB;
+  const uint32_t nY = a_small ? b.nB : b.nA;
+  const uint64_t dx = dsum(X, nX);
+  if (!(c.tune & 1u)) {
+    const float wa = fminf(1.f, (static_cast<float>(b.A[b.nA - 1] - b.A[0]) + 1.f) / c.nv);
+    const float wb = fminf(1.f, (static_cast<float>(b.B[b.nB - 1] - b.B[0]) + 1.f) / c.nv);
+    const float wx = a_small ? wb : wa, wy = a_small ? wa : wb;  // window the other side clips to
+    const float cost_x = kListCost * nX + static_cast<float>(dx) * wx;
+    const float cost_y_min = (kListCost + wy) * nY;
+    if (cost_y_min >= cost_x) {
+      sum_s = dx;
+      return !a_small;
+    }
+  }
+  const uint64_t dy = dsum(a_small ? b.B : b.A, nY);
+  const bool flip = stream_b_cheaper(c, b, a_small ? dx : dy, a_small ? dy : dx);
+  sum_s = flip ? (a_small ? dy : dx) : (a_small ? dx : dy);
+  return flip;
+}
+
 struct HeavyQueue {
   uint32_t* items;          // kHeavyItemWords per item
   unsigned long long cap;
@@ -710,9 +807,8 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
     if (b.same) {
       sum_s = 0;
     } else {
-      const uint64_t da = degree_sum(c, b.A, b.nA, 0, 32), db = degree_sum(c, b.B, b.nB, 0, 32);
-      flip = stream_b_cheaper(c, b, da, db);
-      sum_s = flip ? db : da;
+      flip = choose_stream_b(c, b, [&](const uint32_t* X, uint32_t n) { return degree_sum(c, X, n, 0, 32); },
+                             sum_s);
     }
     ProbeSet ps;
     ps.arr = flip ? b.A : b.B;
@@ -721,11 +817,12 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
     ps.hi = ps.arr[ps.n - 1];
     ps.hash = c.hash;
     ps.bits = 0;
-    if (ps.n * 2 > kHashSlots) {
-      // Too big for the warp's table.  Queue it for the CTA tier unless the
-      // streaming side is trivially small (then binary search is cheaper).
-      if (b.same) sum_s = degree_sum(c, b.A, b.nA, 0, 32);
-      if (sum_s > kHeavyMinStream && hq.items) {
+    if (b.same && (ps.n * 2 > kHashSlots || c.heavy_stream)) sum_s = degree_sum(c, b.A, b.nA, 0, 32);
+    if (ps.n * 2 > kHashSlots || (c.heavy_stream && sum_s >= c.heavy_stream)) {
+      // Too big for the warp's table (or a long stream).  Queue it for the CTA
+      // tier unless the streaming side is trivially small (then binary search
+      // is cheaper).
+      if (sum_s > c.heavy_min && hq.items) {
         unsigned long long slot = 0;
         if (c.lane == 0) slot = atomicAdd(hq.count, 1ull);
         slot = __shfl_sync(kFull, slot, 0);
@@ -736,7 +833,8 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
           return 0;
         }
       }
-    } else {
+    }
+    if (ps.n * 2 <= kHashSlots) {
       ps.bits = table_bits(ps.n);
       __syncwarp();
       fill_table(c.hash, ps, c.lane, 32);
@@ -1017,7 +1115,10 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) 
   c.lane = lane;
   c.nv = static_cast<float>(a.nverts);
   c.tune = a.tune;
+  c.heavy_stream = a.heavy_stream;
+  c.heavy_min = a.heavy_min;
   c.hash = dyn_smem + wib * kHashSlots;
+  c.desc = dyn_smem + kWarpsPerBlock * kHashSlots + wib * kDescWords;
   const bool batch = P.batch;
   HeavyQueue hq;
   hq.items = a.heavy_items;
@@ -1178,6 +1279,8 @@ struct HeavyShared {
   uint32_t llo[kTile], lhi[kTile];
   uint32_t search_idx[kTile];
   uint32_t nsearch;
+  uint32_t coffs[kTile + 1];  // long-list chunk offsets (cta_stream)
+  uint32_t llen[kTile];        // long-list lengths (cta_stream)
 };
 
 // Block-wide exclusive scan of one value per thread; *total gets the sum.
@@ -1310,6 +1413,21 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
 
 // CTA-wide load-balanced stream: sum_{s in S} |N(s) & [lo_s, hi_s) & P|.
 // Returns this thread's partial count.
+__device__ __forceinline__ bool probe_bitmap(const ProbeSet& P, uint32_t y) {
+  const uint32_t d = y - P.bm_base;
+  return (P.bm[d >> 5] >> (d & 31)) & 1u;
+}
+
+constexpr uint32_t kCtaLong = 256;          // lists this long are streamed in warp chunks
+constexpr uint32_t kCtaChunk = 1024;  // elements per warp chunk (4 rounds of 8 coalesced loads)
+
+// CTA-wide stream: sum_{s in S} |N(s) & [lo_s, hi_s) & P| with P a bitmap.
+// Per tile of kTile lists every thread resolves one list's window (prefix
+// truncation by binary search on both ends).  Long lists are cut into
+// kCtaChunk-element chunks that whole warps stream with coalesced loads (one
+// owner search per chunk); short lists are expanded by a load-balanced
+// search (runs of kLbsRun elements per thread); skewed pairs binary-search
+// P's window into N(s).  Returns this thread's partial count.
 template <bool TRACE>
 __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, const ProbeSet& P,
                                int rel, HeavyShared& sh, uint64_t* tr) {
@@ -1332,8 +1450,14 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
         if (last >= lo_val && first < hi_val) {
           uint32_t end = deg;
           if (deg > 32) {
-            if (first < lo_val) start = lower_bound_dev(base, deg, lo_val);
-            if (last >= hi_val) end = lower_bound_dev(base, deg, hi_val);
+            // Window ends by binary search (a chain of dependent loads), unless
+            // the part outside the window is small enough to stream and filter
+            // (ids spread evenly over a list's value range).
+            const float span = static_cast<float>(last - first) + 1.f;
+            if (first < lo_val && static_cast<float>(lo_val - first) > span * 0.0625f)
+              start = lower_bound_dev(base, deg, lo_val);
+            if (last >= hi_val && static_cast<float>(last - hi_val) > span * 0.0625f)
+              end = lower_bound_dev(base, deg, hi_val);
           }
           len = end > start ? end - start : 0u;
         }
@@ -1342,16 +1466,52 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
     __syncthreads();  // nsearch reset visible
     const bool search = len > kLongList && static_cast<uint64_t>(P.n) * ilog2p1(len) * 2u < len;
     if (search) sh.search_idx[atomicAdd(&sh.nsearch, 1u)] = threadIdx.x;
-    const uint32_t slen = search ? 0u : len;
-    uint32_t total;
+    const bool is_long = !search && len >= kCtaLong;
+    const uint32_t slen = search || is_long ? 0u : len;
+    const uint32_t nch = is_long ? (len + kCtaChunk - 1) / kCtaChunk : 0u;
+    uint32_t total, tch;
     const uint32_t off = cta_excl_scan(slen, sh, &total);
+    const uint32_t coff = cta_excl_scan(nch, sh, &tch);
     sh.offs[threadIdx.x] = off;
-    if (threadIdx.x == 0) sh.offs[kTile] = total;
+    sh.coffs[threadIdx.x] = coff;
+    if (threadIdx.x == 0) {
+      sh.offs[kTile] = total;
+      sh.coffs[kTile] = tch;
+    }
     sh.lptr[threadIdx.x] = base + start;
     sh.llo[threadIdx.x] = lo_val;
     sh.lhi[threadIdx.x] = hi_val;
+    sh.llen[threadIdx.x] = len;
     __syncthreads();
-    if (TRACE && threadIdx.x == 0) tr[kTrStreamElems] += total;
+    if (TRACE && threadIdx.x == 0) {
+      tr[kTrHeavyElems] += total;
+      tr[kTrHeavyTiles] += 1;
+    }
+    // 1) long lists, one warp per chunk
+    for (uint32_t q = warp; q < tch; q += kHeavyWarps) {
+      uint32_t j = 0;
+#pragma unroll
+      for (uint32_t step = kTile / 2; step >= 1; step >>= 1)
+        if (sh.coffs[j + step] <= q) j += step;
+      const uint32_t* lp = sh.lptr[j];
+      const uint32_t ll = sh.llen[j], jlo = sh.llo[j], jhi = sh.lhi[j];
+      const uint32_t e0 = (q - sh.coffs[j]) * kCtaChunk;
+      const uint32_t e1 = min(ll, e0 + kCtaChunk);
+      if (TRACE && lane == 0) tr[kTrStreamElems] += e1 - e0;
+      constexpr int kU = 8;  // loads in flight per lane
+      for (uint32_t t = e0 + lane; t < e1; t += 32 * kU) {
+        uint32_t y[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          const uint32_t idx = t + 32 * k;
+          y[k] = idx < e1 ? __ldg(lp + idx) : kEmptySlot;
+        }
+#pragma unroll
+        for (int k = 0; k < kU; ++k)
+          if (y[k] >= jlo && y[k] < jhi && probe_bitmap(P, y[k])) ++hits;
+      }
+    }
+    // 2) short lists: load-balanced runs
     for (uint32_t e0 = threadIdx.x * kLbsRun; e0 < total; e0 += kTile * kLbsRun) {
       // owner of e0: the last j with offs[j] <= e0; its list state is kept in
       // registers and reloaded only when the run crosses into the next list
@@ -1384,16 +1544,12 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
       }
 #pragma unroll
       for (int k = 0; k < kLbsRun; ++k)
-        if (y[k] >= ylo[k] && y[k] < yhi[k] && probe(P, y[k])) ++hits;
+        if (y[k] >= ylo[k] && y[k] < yhi[k] && probe_bitmap(P, y[k])) ++hits;
     }
-    // skewed pairs: one warp per list, P's window binary-searched into N(s)
+    // 3) skewed pairs: one warp per list, P's window binary-searched into N(s)
     for (uint32_t q = warp; q < sh.nsearch; q += kHeavyWarps) {
       const uint32_t jt = sh.search_idx[q];
-      const uint32_t* jb = sh.lptr[jt];
-      const uint32_t jl = (jt + 1 < kTile ? 0u : 0u);
-      (void)jl;
       const uint32_t jlo = sh.llo[jt], jhi = sh.lhi[jt];
-      // the list's length was not kept in smem: recompute from its window
       const uint32_t pa = lower_bound_rw(P.arr, P.n, jlo);
       const uint32_t pb = lower_bound_rw(P.arr, P.n, jhi);
       const uint32_t s = S[tile + jt];
@@ -1402,7 +1558,6 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
       const uint32_t deg = static_cast<uint32_t>(e - b);
       for (uint32_t qq = pa + lane; qq < pb; qq += 32)
         if (contains_dev(lb, deg, P.arr[qq])) ++hits;
-      (void)jb;
     }
     __syncthreads();
   }
@@ -1410,10 +1565,14 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
 }
 
 template <bool TRACE>
-__global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(kHeavyThreads, 1) heavy_kernel(const KernelArgs a) {
   __shared__ HeavyShared sh;
   extern __shared__ uint4 table4[];
-  uint32_t* table = reinterpret_cast<uint32_t*>(table4);
+  // dynamic smem: [bitmap, kBitmapWords) [node table / clique-local region)
+  uint32_t* bm = reinterpret_cast<uint32_t*>(table4);
+  uint32_t* table = bm + kBitmapWords;
+  for (uint32_t i = threadIdx.x; i < kBitmapWords / 4; i += kHeavyThreads)
+    table4[i] = make_uint4(0u, 0u, 0u, 0u);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const Program& P = a.prog;
@@ -1426,7 +1585,10 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
   c.lane = lane;
   c.nv = static_cast<float>(a.nverts);
   c.tune = a.tune;
+  c.heavy_stream = 0;
+  c.heavy_min = 0;
   c.hash = table;
+  c.desc = nullptr;
   uint64_t trbuf[TRACE ? kTrCount : 1];
   if (TRACE)
     for (int i = 0; i < kTrCount; ++i) trbuf[i] = 0;
@@ -1489,19 +1651,17 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
     // side choice from the degree sums (CTA-wide)
     bool flip = false;
     if (!b.same) {
-      const uint64_t da = degree_sum(c, b.A, b.nA, warp * 32, kHeavyThreads);
-      const uint64_t db = degree_sum(c, b.B, b.nB, warp * 32, kHeavyThreads);
-      if (lane == 0) {
-        sh.red_a[warp] = da;
-        sh.red_b[warp] = db;
-      }
-      __syncthreads();
-      uint64_t sa = 0, sb = 0;
-      for (int w = 0; w < kHeavyWarps; ++w) {
-        sa += sh.red_a[w];
-        sb += sh.red_b[w];
-      }
-      flip = stream_b_cheaper(c, b, sa, sb);
+      uint64_t sum_s = 0;
+      auto cta_dsum = [&](const uint32_t* X, uint32_t n) -> uint64_t {
+        const uint64_t d = degree_sum(c, X, n, warp * 32, kHeavyThreads);
+        __syncthreads();
+        if (lane == 0) sh.red_a[warp] = d;
+        __syncthreads();
+        uint64_t t = 0;
+        for (int w = 0; w < kHeavyWarps; ++w) t += sh.red_a[w];
+        return t;
+      };
+      flip = choose_stream_b(c, b, cta_dsum, sum_s);
       __syncthreads();
     }
     const uint32_t* Parr = flip ? b.A : b.B;
@@ -1510,9 +1670,34 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
     const uint32_t nS = flip ? b.nB : b.nA;
     const int rel = yltx ? (flip ? 2 : 1) : 0;
     uint64_t core = 0;
-    for (uint32_t pc = 0; pc < Pn; pc += kHeavyChunk) {
-      const ProbeSet ps = cta_table(table, Parr + pc, min(kHeavyChunk, Pn - pc));
+    // The probe set as a bitmap, one id slice of kBitmapSpan at a time (one
+    // slice whenever n <= 2^20); the streamed lists are clipped to the slice's
+    // part of P, so every element is probed once.
+    for (uint32_t i0 = 0; i0 < Pn;) {
+      const uint32_t base = Parr[i0];
+      const uint64_t lim = static_cast<uint64_t>(base) + kBitmapSpan;
+      const uint32_t i1 = static_cast<uint64_t>(Parr[Pn - 1]) < lim
+                              ? Pn
+                              : i0 + lower_bound_rw(Parr + i0, Pn - i0, static_cast<uint32_t>(lim));
+      for (uint32_t i = i0 + threadIdx.x; i < i1; i += kHeavyThreads) {
+        const uint32_t d = Parr[i] - base;
+        atomicOr(&bm[d >> 5], 1u << (d & 31));
+      }
+      __syncthreads();
+      ProbeSet ps;
+      ps.arr = Parr + i0;
+      ps.n = i1 - i0;
+      ps.lo = Parr[i0];
+      ps.hi = Parr[i1 - 1];
+      ps.hash = nullptr;
+      ps.bits = 0;
+      ps.bm = bm;
+      ps.bm_base = base;
       core += cta_stream<TRACE>(c, S, nS, ps, rel, sh, tr);
+      __syncthreads();
+      for (uint32_t i = i0 + threadIdx.x; i < i1; i += kHeavyThreads) bm[(Parr[i] - base) >> 5] = 0u;
+      __syncthreads();
+      i0 = i1;
     }
     core = warp_sum64(core);
     if (TRACE && threadIdx.x == 0) tr[kTrHeavyStream] += clock64() - t1;
@@ -1553,7 +1738,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 4) heavy_kernel(const KernelArg
   if (TRACE && lane == 0) {
     for (int i = 0; i < kTrCount; ++i)
       if (tr[i] && ((i != kTrHeavyItems && i != kTrHeavyCycles && i != kTrHeavyBuild &&
-                     i != kTrHeavyStream) || threadIdx.x == 0))
+                     i != kTrHeavyStream && i != kTrHeavyElems && i != kTrHeavyTiles) || threadIdx.x == 0))
         atomicAdd(&a.ctr->trace[i], static_cast<unsigned long long>(tr[i]));
   }
 }
@@ -1586,7 +1771,10 @@ __global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint
   c.lane = lane;
   c.nv = static_cast<float>(a.nverts);
   c.tune = a.tune;
+  c.heavy_stream = a.heavy_stream;
+  c.heavy_min = a.heavy_min;
   c.hash = dyn_smem + wib * kHashSlots;
+  c.desc = dyn_smem + kWarpsPerBlock * kHashSlots + wib * kDescWords;
   uint32_t* leafbuf = c.scratch + static_cast<uint64_t>(P.nslots) * a.cap;
   WarpState& s = states[wib];
   const int n = P.depth;
@@ -1703,6 +1891,14 @@ thread_local std::string g_last_error;
 const uint32_t g_tune = [] {
   const char* e = std::getenv("SMG_TUNE");
   return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+}();
+const uint32_t g_heavy_stream = [] {
+  const char* e = std::getenv("SMG_HEAVY_STREAM");
+  return e ? static_cast<uint32_t>(std::atol(e)) : 0u;
+}();
+const uint32_t g_heavy_min = [] {
+  const char* e = std::getenv("SMG_HEAVY_MIN");
+  return e ? static_cast<uint32_t>(std::atol(e)) : static_cast<uint32_t>(kHeavyMinStream);
 }();
 const int g_trace = [] {
   const char* e = std::getenv("SMG_TRACE");
@@ -1842,6 +2038,8 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.unit_end = L.unit_end;
   a.nverts = g.n;
   a.tune = g_tune;
+  a.heavy_stream = g_heavy_stream;
+  a.heavy_min = g_heavy_min;
   a.shard = L.shard;
   a.num_shards = L.num_shards;
   a.ctr = r.ctr;
@@ -1854,12 +2052,12 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   if (L.unit_end > L.unit_begin) {
     count_kernel<METER, TRACE><<<static_cast<unsigned>(blocks), kThreads, kDynSmem, st>>>(a);
     if (heavy) {
-      const size_t hsm = clique ? std::max(kHeavySmem, kHeavyCliqueSmem) : kHeavySmem;
+      const size_t hsm = clique ? std::max(kHeavySmem, kBitmapWords * 4 + kHeavyCliqueSmem) : kHeavySmem;
       SMG_CUDA(cudaFuncSetAttribute(heavy_kernel<TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hsm)));
       int hper = 0;
       SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hper, heavy_kernel<TRACE>, kHeavyThreads, hsm));
-      hper = std::min(4, std::max(1, hper));
+      hper = std::min(1, std::max(1, hper));
       heavy_kernel<TRACE><<<r.num_sms * hper, kHeavyThreads, hsm, st>>>(a);
     }
   }
@@ -1892,7 +2090,8 @@ int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* 
                                           "leaves", "bigP_stream_cycles", "deferred",
                                           "heavy_items", "heavy_cycles", "long_lists",
                                           "heavy_build_cycles", "heavy_stream_cycles",
-                                          "warp_busy_sum_ns", "warp_busy_max_ns"};
+                                          "warp_busy_sum_ns", "warp_busy_max_ns", "heavy_elems",
+                                          "heavy_tiles"};
     std::fprintf(stderr, "[smg trace] kernel %.3f ms:", t);
     for (int i = 0; i < kTrCount; ++i)
       std::fprintf(stderr, " %s=%.4g", names[i], static_cast<double>(r.host_ctr->trace[i]));
@@ -2287,6 +2486,8 @@ int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has
   a.ctr = r.ctr;
   a.nverts = g->n;
   a.tune = g_tune;
+  a.heavy_stream = g_heavy_stream;
+  a.heavy_min = g_heavy_min;
   a.prog = prog;
   unsigned long long total = 0;
   int status = SMG_OK;

@@ -149,6 +149,25 @@ def test_cfg2_reference_root_windows(golden_configs, cfg2):
             assert count_range(cfg2, plan, w["lo"], w["hi"]).count == w["count"], (label, w)
 
 
+def test_cfg2_hub_roots(golden_configs, cfg2):
+    """Per-root reference counts of cfg2's highest-degree roots: these units
+    run through the CTA tier (bitmap probe sets) and the big-set paths."""
+    hubs = golden_configs["cfg2"].get("hub_roots")
+    if not hubs:
+        pytest.skip("hub_roots not generated (tools/ref_full_cfg2.py)")
+    for label, plan in configs.config_patterns("cfg2"):
+        rec = hubs[label]
+        got = [count_range(cfg2, plan, v, v + 1).count for v in rec["roots"]]
+        assert got == rec["counts"], label
+
+
+def test_cfg2_full_clique4_vs_reference(golden_configs, cfg2):
+    full = golden_configs["cfg2"]["full"].get("clique4")
+    if not full:
+        pytest.skip("full reference count not generated")
+    assert count(cfg2, named_plan("clique", 4)) == full["count"]
+
+
 def test_cfg2_full_size_invariants(cfg2):
     p = named_plan("clique", 4)
     full = count_result(cfg2, p)
