@@ -39,11 +39,16 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr uint32_t kChunk = 32;  // edge slots per queue grab
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kHashLog2 = 11;  // per-warp shared-memory hash: 2048 slots (8 KB)
+#ifndef SMG_HASH_LOG2
+#define SMG_HASH_LOG2 9
+#endif
+#ifndef SMG_COUNT_MINB
+#define SMG_COUNT_MINB 8
+#endif
+constexpr int kHashLog2 = SMG_HASH_LOG2;  // per-warp shared-memory hash: 512 slots (2 KB)
 constexpr uint32_t kHashSlots = 1u << kHashLog2;
 constexpr uint32_t kEmptySlot = 0xffffffffu;  // never a vertex id (ids < n < 2^32)
-constexpr uint32_t kDescWords = 168;  // excl[33] lo[32] hi[32] ptr[32] (8-byte aligned)
-constexpr size_t kDynSmem = sizeof(uint32_t) * (kHashSlots + kDescWords) * kWarpsPerBlock;
+constexpr size_t kDynSmem = sizeof(uint32_t) * kHashSlots * kWarpsPerBlock;
 // CTA tier (heavy_kernel): one 32-warp CTA per SM.  Node builds probe a
 // 8K-slot (32 KB) hash table; the batched leaf probes a 1M-bit (128 KB)
 // bitmap of the probe set over an id slice.
@@ -53,7 +58,7 @@ constexpr uint32_t kHeavySlots = 1u << 13;
 constexpr uint32_t kBitmapWords = 1u << 15;                 // 128 KB
 constexpr uint64_t kBitmapSpan = uint64_t(kBitmapWords) * 32;  // ids per slice
 constexpr size_t kHeavySmem = sizeof(uint32_t) * (kHeavySlots + kBitmapWords);
-constexpr uint64_t kHeavyMinStream = 32768;  // defer only batches with real streaming work
+constexpr uint64_t kHeavyMinStream = 65536;  // defer only batches with real streaming work
 constexpr uint64_t kHeavyQueueCap = 1ull << 24;
 
 // ---------------------------------------------------------------- device ---
@@ -154,6 +159,85 @@ __device__ __forceinline__ uint32_t lower_bound_rw(const uint32_t* a, uint32_t n
   return static_cast<uint32_t>(base - a) + (*base < x ? 1u : 0u);
 }
 
+// Warp-cooperative lower_bound for a warp-uniform query (every lane gets the
+// answer): a 32-ary search, one round of 32 independent pivot loads + ballot
+// per factor of 32 (64K-element list: 3 rounds + 1) instead of a 16-step
+// chain of dependent loads.  All 32 lanes must call it.  LDG: read-only
+// (CSR) data through the non-coherent path.
+template <bool LDG>
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t n, uint32_t x) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t idx = min(lo + (lane + 1) * step - 1, hi - 1);
+    const uint32_t v = LDG ? __ldg(a + idx) : a[idx];
+    const int cnt = __popc(__ballot_sync(0xffffffffu, v < x));  // pivots below x (a prefix)
+    const uint32_t nlo = cnt ? min(lo + cnt * step, hi) : lo;
+    const uint32_t nhi = cnt < 32 ? min(lo + (cnt + 1) * step - 1, hi - 1) : hi;
+    lo = nlo;
+    hi = max(nhi, nlo);
+  }
+  const uint32_t idx = lo + lane;
+  const bool lt = idx < hi && (LDG ? __ldg(a + idx) : a[idx]) < x;
+  return lo + __popc(__ballot_sync(0xffffffffu, lt));
+}
+
+// CTA-cooperative version (all threads of the block must call it; contains
+// barriers): a blockDim-ary search, e.g. 2 rounds for a 64K-element list.
+template <bool LDG>
+__device__ __forceinline__ uint32_t cta_lower_bound(const uint32_t* a, uint32_t n, uint32_t x) {
+  const uint32_t nt = blockDim.x, t = threadIdx.x;
+  uint32_t lo = 0, hi = n;
+  while (hi - lo > nt) {
+    const uint32_t step = (hi - lo + nt - 1) / nt;
+    const uint32_t idx = min(lo + (t + 1) * step - 1, hi - 1);
+    const uint32_t v = LDG ? __ldg(a + idx) : a[idx];
+    const uint32_t cnt = __syncthreads_count(v < x);
+    const uint32_t nlo = cnt ? min(lo + cnt * step, hi) : lo;
+    const uint32_t nhi = cnt < nt ? min(lo + (cnt + 1) * step - 1, hi - 1) : hi;
+    lo = nlo;
+    hi = max(nhi, nlo);
+  }
+  const uint32_t idx = lo + t;
+  const bool lt = idx < hi && (LDG ? __ldg(a + idx) : a[idx]) < x;
+  return lo + __syncthreads_count(lt);
+}
+
+// Window ends of a sorted neighbour list without a bisection chain.  Ids are
+// spread evenly over a list's value range (the configs permute ids), so the
+// rank of a bound is predicted from the end values; one load at the
+// prediction minus (plus) a margin of a few standard deviations proves a
+// safe index, and only a failed check falls back to bisection.  The returned
+// window may include a few elements outside [lo, hi): callers filter each
+// element against the window anyway.
+//   window_start: i with a[j] < lo for all j < i  (requires a[0] < lo)
+//   window_end:   e with a[j] >= hi for all j >= e (requires a[n-1] >= hi)
+__device__ __forceinline__ uint32_t guess_margin(uint32_t n) {
+  return 8u + 2u * static_cast<uint32_t>(sqrtf(static_cast<float>(n)));
+}
+
+__device__ __forceinline__ uint32_t window_start(const uint32_t* a, uint32_t n, uint32_t first,
+                                                 uint32_t last, uint32_t lo) {
+  const float f = static_cast<float>(lo - first) / (static_cast<float>(last - first) + 1.f);
+  const uint32_t g = static_cast<uint32_t>(f * static_cast<float>(n));
+  const uint32_t m = guess_margin(n);
+  if (g <= m) return 0u;
+  const uint32_t i = g - m;
+  if (__ldg(a + i) < lo) return i;
+  return lower_bound_dev(a, i, lo);
+}
+
+__device__ __forceinline__ uint32_t window_end(const uint32_t* a, uint32_t n, uint32_t first,
+                                               uint32_t last, uint32_t hi) {
+  const float f = static_cast<float>(hi - first) / (static_cast<float>(last - first) + 1.f);
+  const uint32_t g = static_cast<uint32_t>(f * static_cast<float>(n));
+  const uint32_t e = g + guess_margin(n);
+  if (e >= n - 1) return n;
+  if (__ldg(a + e) >= hi) return e;
+  return e + 1 + lower_bound_dev(a + e + 1, n - e - 1, hi);
+}
+
 struct Ctx {
   const unsigned long long* __restrict__ off;
   const uint32_t* __restrict__ adj;
@@ -165,7 +249,6 @@ struct Ctx {
   float nv;  // number of vertices (id range), for window-fraction estimates
   uint32_t tune;
   uint32_t heavy_stream;  // defer batches streaming at least this many elements (0: off)
-  uint32_t* desc;         // per-warp list-descriptor area (kDescWords), warp tier only
   uint32_t heavy_min;     // defer big-probe-set batches only above this streamed degree sum
 };
 
@@ -308,22 +391,22 @@ __device__ __forceinline__ bool prefer_stream(uint32_t small, uint32_t large) {
 
 // Stream X[0..nX), keep x iff (x in Pr) == keep_found and x != exclude.
 // COUNT: return the number kept; else also write them, in order, to out.
-template <bool COUNT>
+template <bool COUNT, int U = kUnroll>
 __device__ uint32_t filter_list(const Ctx& c, const uint32_t* X, uint32_t nX, const ProbeSet& Pr,
                                 bool keep_found, uint32_t exclude, uint32_t* out) {
   const unsigned lt_mask = (1u << c.lane) - 1u;
   uint32_t written = 0;
-  for (uint32_t base = 0; base < nX; base += 32 * kUnroll) {
-    uint32_t x[kUnroll];
-    bool ok[kUnroll];
+  for (uint32_t base = 0; base < nX; base += 32 * U) {
+    uint32_t x[U];
+    bool ok[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t i = base + u * 32 + c.lane;
       ok[u] = i < nX;
       x[u] = ok[u] ? X[i] : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       bool keep = ok[u] && x[u] != exclude;
       if (keep) keep = probe(Pr, x[u]) == keep_found;
       const unsigned m = __ballot_sync(kFull, keep);
@@ -347,7 +430,7 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
     uint32_t nL;
     nbrs(c, v, L, nL);
     if (nd.ops[0].mode == kOpIsect) {
-      if (nd.bound >= 0) nL = lower_bound_dev(L, nL, s.vals[nd.bound]);
+      if (nd.bound >= 0) nL = warp_lower_bound<true>(L, nL, s.vals[nd.bound]);
       if (nL == 0) return 0;
       // result = in & L; iterate either side (both sorted -> sorted output)
       const bool in_small = inlen <= nL;
@@ -364,8 +447,8 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
     }
     // result = in - N[v]: stream `in`; only N(v) within [in.lo, in.hi] matters
     const uint32_t lo = in[0], hi = in[inlen - 1];
-    const uint32_t a = lower_bound_dev(L, nL, lo);
-    const uint32_t b = lower_bound_dev(L, nL, hi + 1u);  // independent of a: overlaps
+    const uint32_t a = warp_lower_bound<true>(L, nL, lo);
+    const uint32_t b = a + warp_lower_bound<true>(L + a, nL - a, hi + 1u);
     if (b == a) {  // nothing to subtract but v itself
       ProbeSet none;
       none.arr = L;
@@ -414,7 +497,20 @@ __device__ __forceinline__ void node_input(const Ctx& c, const Node& nd, const u
   } else {
     nbrs(c, s.vals[nd.list], in, inlen);
   }
-  if (nd.bound >= 0) inlen = lower_bound_rw(in, inlen, s.vals[nd.bound]);
+  if (nd.bound >= 0) inlen = warp_lower_bound<false>(in, inlen, s.vals[nd.bound]);
+}
+
+// CTA tier: the same, with a block-cooperative search (all threads call it).
+__device__ __forceinline__ void node_input_cta(const Ctx& c, const Node& nd, const uint32_t*& in,
+                                               uint32_t& inlen) {
+  const WarpState& s = *c.s;
+  if (nd.src >= 0) {
+    in = s.ptr[nd.src];
+    inlen = s.len[nd.src];
+  } else {
+    nbrs(c, s.vals[nd.list], in, inlen);
+  }
+  if (nd.bound >= 0) inlen = cta_lower_bound<false>(in, inlen, s.vals[nd.bound]);
 }
 
 __device__ void build_node(const Ctx& c, const Program& P, int t) {
@@ -517,6 +613,27 @@ constexpr uint32_t kLongList = 64;  // lists this long are streamed by the whole
 // starts below lo); short lists are flattened across the lanes; skewed pairs
 // (|P| log |N(s)| << |N(s)|) binary-search P into N(s).  Returns this warp's
 // partial (all lanes hold it).
+// One long list streamed by the whole warp: KU coalesced loads in flight per
+// lane, window [lo, hi), early exit once the sorted list passes hi.
+template <int KU>
+__device__ __forceinline__ uint32_t stream_long(const Ctx& c, const uint32_t* jp, uint32_t jl, uint32_t jlo,
+                                                uint32_t jhi, const ProbeSet& P, uint64_t* tr) {
+  uint32_t hits = 0;
+  for (uint32_t t0 = 0; t0 < jl; t0 += 32 * KU) {
+    uint32_t y[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const uint32_t idx = t0 + u * 32 + c.lane;
+      y[u] = idx < jl ? __ldg(jp + idx) : kEmptySlot;
+    }
+#pragma unroll
+    for (int u = 0; u < KU; ++u)
+      if (y[u] < jhi && y[u] >= jlo && probe(P, y[u])) ++hits;
+    if (__any_sync(kFull, y[KU - 1] >= jhi)) break;  // sorted: the rest is >= hi
+  }
+  return hits;
+}
+
 template <bool TRACE>
 __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, const ProbeSet& P,
                                  int rel, uint32_t g_first, uint32_t g_stride, uint64_t* tr) {
@@ -539,7 +656,12 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
           len = deg;
           if (deg >= kLongList) {
             is_long = true;
-            if (first < lo_val) start = lower_bound_dev(base, deg, lo_val);
+            // lower window end by binary search only when the part below it
+            // is a sizeable fraction of the list (else it is streamed and
+            // filtered; ids spread evenly over a list's value range)
+            if (first < lo_val && ((c.tune & 16u) ||
+                static_cast<float>(lo_val - first) > (static_cast<float>(last - first) + 1.f) * 0.0625f))
+              start = window_start(base, deg, first, last, lo_val);
             len = deg - start;
             search = static_cast<uint64_t>(P.n) * ilog2p1(len) * 2u < len;
             is_long = !search;
@@ -561,20 +683,13 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
                                __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j)) +
                            __shfl_sync(kFull, start, j);
       const uint32_t jl = __shfl_sync(kFull, len, j);
+      const uint32_t jlo = __shfl_sync(kFull, lo_val, j);
       const uint32_t jhi = __shfl_sync(kFull, hi_val, j);
-      for (uint32_t t0 = 0; t0 < jl; t0 += 32 * kUnroll) {
-        uint32_t y[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const uint32_t idx = t0 + u * 32 + c.lane;
-          y[u] = idx < jl ? __ldg(jp + idx) : kEmptySlot;
-        }
-        if (TRACE && c.lane == 0) tr[kTrStreamElems] += min(32u * kUnroll, jl - t0);
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if (y[u] < jhi && probe(P, y[u])) ++hits;
-        if (__any_sync(kFull, y[kUnroll - 1] >= jhi)) break;  // sorted: the rest is >= hi
-      }
+      if (TRACE && c.lane == 0) tr[kTrStreamElems] += jl;  // upper bound (early exit)
+      if (c.tune & 8u)
+        hits += stream_long<8>(c, jp, jl, jlo, jhi, P, tr);
+      else
+        hits += stream_long<4>(c, jp, jl, jlo, jhi, P, tr);
     }
     // 2) short lists: flattened over the lanes, range-filtered per element
     const uint32_t slen = is_long || search ? 0u : len;
@@ -582,53 +697,6 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
     const uint32_t tot = __shfl_sync(kFull, incl, 31);
     const uint32_t excl = incl - slen;
     if (TRACE) tr[kTrStreamElems] += tot;
-    if (c.tune & 4u) {
-      // list descriptors in shared memory; every lane expands runs of kRun
-      // consecutive elements of the concatenation (one owner search per run)
-      uint32_t* dex = c.desc;
-      uint32_t* dlo = c.desc + 40;
-      uint32_t* dhi = c.desc + 72;
-      const uint32_t** dptr = reinterpret_cast<const uint32_t**>(c.desc + 104);
-      __syncwarp();
-      dex[c.lane] = excl;
-      if (c.lane == 0) dex[32] = tot;
-      dlo[c.lane] = lo_val;
-      dhi[c.lane] = hi_val;
-      dptr[c.lane] = base - excl;
-      __syncwarp();
-      constexpr uint32_t kRun = 4;
-      for (uint32_t t0 = c.lane * kRun; t0 < tot; t0 += 32 * kRun) {
-        int j = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1)
-          if (dex[j + step] <= t0) j += step;
-        const uint32_t* vp = dptr[j];
-        uint32_t lo = dlo[j], hi = dhi[j], nxt = dex[j + 1];
-        uint32_t y[kRun];
-        bool in[kRun];
-#pragma unroll
-        for (uint32_t k = 0; k < kRun; ++k) {
-          const uint32_t e = t0 + k;
-          in[k] = false;
-          y[k] = 0;
-          if (e < tot) {
-            while (nxt <= e) {
-              ++j;
-              vp = dptr[j];
-              lo = dlo[j];
-              hi = dhi[j];
-              nxt = dex[j + 1];
-            }
-            y[k] = __ldg(vp + e);
-            in[k] = y[k] >= lo && y[k] < hi;
-          }
-        }
-#pragma unroll
-        for (uint32_t k = 0; k < kRun; ++k)
-          if (in[k] && probe(P, y[k])) ++hits;
-      }
-      __syncwarp();
-    } else
     for (uint32_t t = 0; t < tot; t += 64) {
       uint32_t y[2], ylo[2], yhi[2];
 #pragma unroll
@@ -675,7 +743,10 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
       const uint32_t* o_list = reinterpret_cast<const uint32_t*>(
                                    __shfl_sync(kFull, reinterpret_cast<unsigned long long>(base), j)) +
                                __shfl_sync(kFull, start, j);
-      if (idx < ptot && contains_dev(o_list, o_len, P.arr[o_pa + (idx - o_ex)])) ++hits;
+      if (idx < ptot) {
+        const uint32_t key = P.arr[o_pa + (idx - o_ex)];
+        if (contains_dev(o_list, o_len, key)) ++hits;
+      }
     }
     total += hits;
   }
@@ -718,7 +789,7 @@ __device__ __forceinline__ BatchSets batch_sets(const WarpState& s, const Progra
   b.nA = s.len[an];
   b.B = s.ptr[bn];
   b.nB = s.len[bn];
-  if (P.batch_fixed_bound >= 0) b.nB = lower_bound_rw(b.B, b.nB, s.vals[P.batch_fixed_bound]);
+  if (P.batch_fixed_bound >= 0) b.nB = warp_lower_bound<false>(b.B, b.nB, s.vals[P.batch_fixed_bound]);
   b.same = an == bn;
   return b;
 }
@@ -869,7 +940,7 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
 // the CTA tier (heavy_kernel) with |U| <= kLocalCtaMax; beyond that the
 // generic path runs.
 
-constexpr uint32_t kLocalWarpMax = 512;
+constexpr uint32_t kLocalWarpMax = kHashSlots / 4;  // keys, index and row buffer fit the warp hash area
 constexpr uint32_t kLocalCtaMax = 4096;
 constexpr uint32_t kLocalCtaSlots = 2 * kLocalCtaMax;            // index table slots
 constexpr uint32_t kLocalRowWords = kLocalCtaMax / 32;           // CTA row stride (words)
@@ -947,7 +1018,7 @@ __device__ void local_row(const Ctx& c, const LocalIndex& L, const uint32_t* U, 
   uint32_t start = 0;
   if (deg && lo < hi) {
     const uint32_t first = __ldg(p);
-    if (first < lo) start = lower_bound_dev(p, deg, lo);
+    if (first < lo) start = warp_lower_bound<true>(p, deg, lo);
     for (uint32_t t0 = start; t0 < deg; t0 += 32 * kUnroll) {
       uint32_t y[kUnroll];
 #pragma unroll
@@ -1093,13 +1164,13 @@ __device__ uint64_t clique_local_warp(const Ctx& c, const Program& P, uint32_t* 
   for (uint32_t a = 0; a < u; ++a)
     local_row(c, L, U, u, a, lower, rowbuf, nwords, rows + static_cast<uint64_t>(a) * kLocalWarpRowWords);
   __syncwarp();
-  const uint32_t q0 = lower_bound_rw(U, u, s.vals[0]);
-  const uint32_t q1 = lower_bound_rw(U, u, s.vals[1]);
+  const uint32_t q0 = warp_lower_bound<false>(U, u, s.vals[0]);
+  const uint32_t q1 = warp_lower_bound<false>(U, u, s.vals[1]);
   return local_dfs<1>(c, P, rows, kLocalWarpRowWords, u, q0, q1, 0, 1);
 }
 
 template <bool METER, bool TRACE>
-__global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(kThreads, SMG_COUNT_MINB) count_kernel(const KernelArgs a) {
   __shared__ WarpState states[kWarpsPerBlock];
   extern __shared__ uint32_t dyn_smem[];
   const int lane = threadIdx.x & 31;
@@ -1118,7 +1189,6 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const KernelArgs a) 
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.hash = dyn_smem + wib * kHashSlots;
-  c.desc = dyn_smem + kWarpsPerBlock * kHashSlots + wib * kDescWords;
   const bool batch = P.batch;
   HeavyQueue hq;
   hq.items = a.heavy_items;
@@ -1326,7 +1396,7 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t* in;
   uint32_t inlen;
-  node_input(c, nd, in, inlen);
+  node_input_cta(c, nd, in, inlen);
   if (nd.raw || nd.nops != 1) {
     if (warp == 0) build_node(c, P, t);  // raw slice, or a multi-op start node (rare)
     __syncthreads();
@@ -1349,7 +1419,7 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
   if (inlen == 0) {
     nX = 0;
   } else if (nd.ops[0].mode == kOpIsect) {
-    if (nd.bound >= 0) nL = lower_bound_dev(L, nL, s.vals[nd.bound]);
+    if (nd.bound >= 0) nL = cta_lower_bound<true>(L, nL, s.vals[nd.bound]);
     if (nL == 0) {
       nX = 0;
     } else {
@@ -1378,8 +1448,8 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
   } else {
     keep_found = false;
     exclude = v;
-    const uint32_t a = lower_bound_dev(L, nL, in[0]);
-    const uint32_t b = lower_bound_dev(L, nL, in[inlen - 1] + 1u);
+    const uint32_t a = cta_lower_bound<true>(L, nL, in[0]);
+    const uint32_t b = a + cta_lower_bound<true>(L + a, nL - a, in[inlen - 1] + 1u);
     if (b > a) {
       if (2 * (b - a) <= kHeavySlots) {
         pr = cta_table(table, L + a, b - a);
@@ -1392,9 +1462,9 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
     }
   }
   // two passes over per-warp slices: count, scan, write in order
-  const uint32_t chunk = ((nX + kHeavyWarps - 1) / kHeavyWarps + 127) / 128 * 128;
+  const uint32_t chunk = ((nX + kHeavyWarps - 1) / kHeavyWarps + 255) / 256 * 256;
   const uint32_t lo = min(nX, warp * chunk), hi = min(nX, lo + chunk);
-  const uint32_t cnt = filter_list<true>(c, X + lo, hi - lo, pr, keep_found, exclude, nullptr);
+  const uint32_t cnt = filter_list<true, 8>(c, X + lo, hi - lo, pr, keep_found, exclude, nullptr);
   if (lane == 0) sh.wsum[warp] = cnt;
   __syncthreads();
   uint32_t off = 0, total = 0;
@@ -1402,7 +1472,7 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
     off += w < warp ? sh.wsum[w] : 0u;
     total += sh.wsum[w];
   }
-  filter_list<false>(c, X + lo, hi - lo, pr, keep_found, exclude, out + off);
+  filter_list<false, 8>(c, X + lo, hi - lo, pr, keep_found, exclude, out + off);
   __syncthreads();
   if (threadIdx.x == 0) {
     sh.st.ptr[t] = out;
@@ -1455,9 +1525,9 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
             // (ids spread evenly over a list's value range).
             const float span = static_cast<float>(last - first) + 1.f;
             if (first < lo_val && static_cast<float>(lo_val - first) > span * 0.0625f)
-              start = lower_bound_dev(base, deg, lo_val);
+              start = window_start(base, deg, first, last, lo_val);
             if (last >= hi_val && static_cast<float>(last - hi_val) > span * 0.0625f)
-              end = lower_bound_dev(base, deg, hi_val);
+              end = window_end(base, deg, first, last, hi_val);
           }
           len = end > start ? end - start : 0u;
         }
@@ -1550,8 +1620,8 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
     for (uint32_t q = warp; q < sh.nsearch; q += kHeavyWarps) {
       const uint32_t jt = sh.search_idx[q];
       const uint32_t jlo = sh.llo[jt], jhi = sh.lhi[jt];
-      const uint32_t pa = lower_bound_rw(P.arr, P.n, jlo);
-      const uint32_t pb = lower_bound_rw(P.arr, P.n, jhi);
+      const uint32_t pa = warp_lower_bound<false>(P.arr, P.n, jlo);
+      const uint32_t pb = pa + warp_lower_bound<false>(P.arr + pa, P.n - pa, jhi);
       const uint32_t s = S[tile + jt];
       const unsigned long long b = __ldg(c.off + s), e = __ldg(c.off + s + 1);
       const uint32_t* lb = c.adj + b;
@@ -1588,7 +1658,6 @@ __global__ void __launch_bounds__(kHeavyThreads, 1) heavy_kernel(const KernelArg
   c.heavy_stream = 0;
   c.heavy_min = 0;
   c.hash = table;
-  c.desc = nullptr;
   uint64_t trbuf[TRACE ? kTrCount : 1];
   if (TRACE)
     for (int i = 0; i < kTrCount; ++i) trbuf[i] = 0;
@@ -1626,8 +1695,8 @@ __global__ void __launch_bounds__(kHeavyThreads, 1) heavy_kernel(const KernelArg
         local_row(c, L, U, u, r, lower, rowbuf, nwords, rows + static_cast<uint64_t>(r) * kLocalRowWords);
       __threadfence_block();
       __syncthreads();
-      const uint32_t q0 = lower_bound_rw(U, u, sh.st.vals[0]);
-      const uint32_t q1 = lower_bound_rw(U, u, sh.st.vals[1]);
+      const uint32_t q0 = cta_lower_bound<false>(U, u, sh.st.vals[0]);
+      const uint32_t q1 = cta_lower_bound<false>(U, u, sh.st.vals[1]);
       const uint64_t part = local_dfs<kLocalRowWords / 32>(c, P, rows, kLocalRowWords, u, q0, q1, warp,
                                                           kHeavyWarps);
       if (lane == 0) sh.red_a[warp] = part;
@@ -1678,7 +1747,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 1) heavy_kernel(const KernelArg
       const uint64_t lim = static_cast<uint64_t>(base) + kBitmapSpan;
       const uint32_t i1 = static_cast<uint64_t>(Parr[Pn - 1]) < lim
                               ? Pn
-                              : i0 + lower_bound_rw(Parr + i0, Pn - i0, static_cast<uint32_t>(lim));
+                              : i0 + cta_lower_bound<false>(Parr + i0, Pn - i0, static_cast<uint32_t>(lim));
       for (uint32_t i = i0 + threadIdx.x; i < i1; i += kHeavyThreads) {
         const uint32_t d = Parr[i] - base;
         atomicOr(&bm[d >> 5], 1u << (d & 31));
@@ -1774,7 +1843,6 @@ __global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.hash = dyn_smem + wib * kHashSlots;
-  c.desc = dyn_smem + kWarpsPerBlock * kHashSlots + wib * kDescWords;
   uint32_t* leafbuf = c.scratch + static_cast<uint64_t>(P.nslots) * a.cap;
   WarpState& s = states[wib];
   const int n = P.depth;
