@@ -49,13 +49,24 @@ constexpr int kHashLog2 = SMG_HASH_LOG2;  // per-warp shared-memory hash: 512 sl
 constexpr uint32_t kHashSlots = 1u << kHashLog2;
 constexpr uint32_t kEmptySlot = 0xffffffffu;  // never a vertex id (ids < n < 2^32)
 constexpr size_t kDynSmem = sizeof(uint32_t) * kHashSlots * kWarpsPerBlock;
-// CTA tier (heavy_kernel): one 32-warp CTA per SM.  Node builds probe a
-// 8K-slot (32 KB) hash table; the batched leaf probes a 1M-bit (128 KB)
-// bitmap of the probe set over an id slice.
-constexpr int kHeavyWarps = 32;
+// CTA tier (heavy_kernel): two 16-warp CTAs per SM (one can run while the
+// other waits at a barrier).  Node builds probe an 8K-slot (32 KB) hash
+// table; the batched leaf probes a 512K-bit (64 KB) bitmap of the probe set
+// over an id slice.
+#ifndef SMG_HEAVY_WARPS
+#define SMG_HEAVY_WARPS 16
+#endif
+#ifndef SMG_BITMAP_LOG2
+#define SMG_BITMAP_LOG2 14
+#endif
+constexpr int kHeavyWarps = SMG_HEAVY_WARPS;
 constexpr int kHeavyThreads = kHeavyWarps * 32;
+#ifndef SMG_HEAVY_MINB
+#define SMG_HEAVY_MINB 2
+#endif
+constexpr int kHeavyMinBlocks = SMG_HEAVY_MINB;             // CTAs per SM
 constexpr uint32_t kHeavySlots = 1u << 13;
-constexpr uint32_t kBitmapWords = 1u << 15;                 // 128 KB
+constexpr uint32_t kBitmapWords = 1u << SMG_BITMAP_LOG2;    // 64 KB
 constexpr uint64_t kBitmapSpan = uint64_t(kBitmapWords) * 32;  // ids per slice
 constexpr size_t kHeavySmem = sizeof(uint32_t) * (kHeavySlots + kBitmapWords);
 constexpr uint64_t kHeavyMinStream = 65536;  // defer only batches with real streaming work
@@ -100,6 +111,8 @@ struct KernelArgs {
   unsigned long long heavy_cap;
   uint32_t* heavy_scratch;        // CTA-tier node scratch (nslots * cap per CTA)
   uint32_t* local_rows;           // clique-local rows, warp tier (per warp), or null
+  uint32_t* warp_bitmaps;         // per-warp id bitmaps (bitmap_words each, kept zero), or null
+  uint64_t bitmap_words;
   uint32_t* heavy_rows;           // clique-local rows, CTA tier (per CTA)
   Program prog;
 };
@@ -250,6 +263,7 @@ struct Ctx {
   uint32_t tune;
   uint32_t heavy_stream;  // defer batches streaming at least this many elements (0: off)
   uint32_t heavy_min;     // defer big-probe-set batches only above this streamed degree sum
+  uint32_t* gbm;          // this warp's global bitmap over all ids (zero between uses), or null
 };
 
 __device__ __forceinline__ void nbrs(const Ctx& c, uint32_t v, const uint32_t*& p, uint32_t& len) {
@@ -290,6 +304,8 @@ __device__ __forceinline__ uint32_t hbucket(uint32_t x, int bbits) {
 }
 
 __device__ __forceinline__ bool probe(const ProbeSet& P, uint32_t y) {
+  if (P.bits < 0)  // the warp's global (L2-resident) bitmap; L1 bypassed, it is rewritten per batch
+    return (__ldcg(P.hash + (y >> 5)) >> (y & 31)) & 1u;
   if (P.bits) {
     const int bbits = P.bits - 2;
     const uint32_t mask = (1u << bbits) - 1u;
@@ -905,6 +921,20 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
         }
       }
     }
+    bool global_bm = false;
+    if (ps.n * 2 > kHashSlots && c.gbm) {
+      // Too big for the warp's smem table: a bitmap over all ids in global
+      // memory (L2-resident words), one dependent load per probe instead of
+      // a bisection chain; cleared again below.
+      for (uint32_t i = c.lane; i < ps.n; i += 32) {
+        const uint32_t x = ps.arr[i];
+        atomicOr(c.gbm + (x >> 5), 1u << (x & 31));
+      }
+      __syncwarp();
+      ps.hash = c.gbm;
+      ps.bits = -1;
+      global_bm = true;
+    }
     if (ps.n * 2 <= kHashSlots) {
       ps.bits = table_bits(ps.n);
       __syncwarp();
@@ -922,6 +952,11 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
     long long t0 = TRACE ? clock64() : 0;
     core = flip ? stream_count<TRACE>(c, b.B, b.nB, ps, yltx ? 2 : 0, 0, 32, tr)
                 : stream_count<TRACE>(c, b.A, b.nA, ps, yltx ? 1 : 0, 0, 32, tr);
+    if (global_bm) {
+      __syncwarp();
+      for (uint32_t i = c.lane; i < ps.n; i += 32) c.gbm[ps.arr[i] >> 5] = 0u;
+      __syncwarp();
+    }
     if (TRACE && !ps.bits) tr[kTrBigPCycles] += clock64() - t0;
   }
   if (!P.batch_diff) return core;
@@ -947,7 +982,6 @@ constexpr uint32_t kLocalRowWords = kLocalCtaMax / 32;           // CTA row stri
 constexpr uint32_t kLocalWarpRowWords = kLocalWarpMax / 32;      // warp row stride (words)
 constexpr size_t kHeavyCliqueSmem = kLocalCtaSlots * 4 + kLocalCtaSlots * 2 +
                                     kHeavyWarps * kLocalRowWords * 4;
-constexpr uint16_t kNoIdx = 0xFFFF;
 
 struct LocalIndex {
   uint32_t* keys;   // bucketised like the probe tables
@@ -1082,7 +1116,7 @@ __device__ uint64_t local_dfs(const Ctx& c, const Program& P, const uint32_t* ro
   const int lane = c.lane;
   uint32_t acc[kMaxLevels][WPL];
   uint32_t rem[kMaxLevels][WPL];
-  int a[kMaxLevels];
+  int a[kMaxLevels] = {};
   auto bound_q = [&](int i) -> uint32_t {
     const int p = P.parent[i];
     return p < 0 ? u : (p == 0 ? q0 : (p == 1 ? q1 : static_cast<uint32_t>(a[p])));
@@ -1188,6 +1222,7 @@ __global__ void __launch_bounds__(kThreads, SMG_COUNT_MINB) count_kernel(const K
   c.tune = a.tune;
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
+  c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
   c.hash = dyn_smem + wib * kHashSlots;
   const bool batch = P.batch;
   HeavyQueue hq;
@@ -1635,7 +1670,7 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
 }
 
 template <bool TRACE>
-__global__ void __launch_bounds__(kHeavyThreads, 1) heavy_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(kHeavyThreads, kHeavyMinBlocks) heavy_kernel(const KernelArgs a) {
   __shared__ HeavyShared sh;
   extern __shared__ uint4 table4[];
   // dynamic smem: [bitmap, kBitmapWords) [node table / clique-local region)
@@ -1657,6 +1692,7 @@ __global__ void __launch_bounds__(kHeavyThreads, 1) heavy_kernel(const KernelArg
   c.tune = a.tune;
   c.heavy_stream = 0;
   c.heavy_min = 0;
+  c.gbm = nullptr;
   c.hash = table;
   uint64_t trbuf[TRACE ? kTrCount : 1];
   if (TRACE)
@@ -1842,6 +1878,7 @@ __global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint
   c.tune = a.tune;
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
+  c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
   c.hash = dyn_smem + wib * kHashSlots;
   uint32_t* leafbuf = c.scratch + static_cast<uint64_t>(P.nslots) * a.cap;
   WarpState& s = states[wib];
@@ -1995,6 +2032,8 @@ struct Replica {
   size_t scratch_bytes = 0;
   uint32_t* heavy_items = nullptr;     // CTA-tier queue
   uint32_t* heavy_scratch = nullptr;
+  uint32_t* warp_bitmaps = nullptr;    // per-warp id bitmaps (zeroed once, kept zero by the kernels)
+  size_t warp_bitmaps_bytes = 0;
   uint32_t* local_rows = nullptr;      // clique-local rows (warp tier)
   size_t local_rows_bytes = 0;
   uint32_t* heavy_rows = nullptr;      // clique-local rows (CTA tier)
@@ -2069,6 +2108,19 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
       r.heavy_scratch_bytes = hs;
     }
   }
+  const uint64_t bm_words = (g.n + 31) / 32;
+  if (prog.batch) {
+    const size_t bytes = blocks * kWarpsPerBlock * bm_words * sizeof(uint32_t);
+    if (r.warp_bitmaps_bytes < bytes) {
+      if (r.warp_bitmaps) cudaFree(r.warp_bitmaps);
+      r.warp_bitmaps = nullptr;
+      r.warp_bitmaps_bytes = 0;
+      SMG_CUDA(cudaMalloc(&r.warp_bitmaps, bytes));
+      SMG_CUDA(cudaMemset(r.warp_bitmaps, 0, bytes));
+      SMG_CUDA(cudaDeviceSynchronize());
+      r.warp_bitmaps_bytes = bytes;
+    }
+  }
   const bool clique = !METER && prog.clique;
   if (clique) {
     const size_t lr = blocks * kWarpsPerBlock * kLocalWarpMax * kLocalWarpRowWords * sizeof(uint32_t);
@@ -2115,6 +2167,8 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.heavy_cap = heavy ? kHeavyQueueCap : 0;
   a.heavy_scratch = r.heavy_scratch;
   a.local_rows = clique ? r.local_rows : nullptr;
+  a.warp_bitmaps = (prog.batch && !(g_tune & 64u)) ? r.warp_bitmaps : nullptr;
+  a.bitmap_words = bm_words;
   a.heavy_rows = clique ? r.heavy_rows : nullptr;
   a.prog = prog;
   if (L.unit_end > L.unit_begin) {
@@ -2125,7 +2179,7 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
                                     static_cast<int>(hsm)));
       int hper = 0;
       SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hper, heavy_kernel<TRACE>, kHeavyThreads, hsm));
-      hper = std::min(1, std::max(1, hper));
+      hper = std::min(kHeavyMinBlocks, std::max(1, hper));
       heavy_kernel<TRACE><<<r.num_sms * hper, kHeavyThreads, hsm, st>>>(a);
     }
   }
@@ -2250,6 +2304,7 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->heavy_items) cudaFree(r->heavy_items);
     if (r->heavy_scratch) cudaFree(r->heavy_scratch);
     if (r->local_rows) cudaFree(r->local_rows);
+    if (r->warp_bitmaps) cudaFree(r->warp_bitmaps);
     if (r->heavy_rows) cudaFree(r->heavy_rows);
     if (r->ctr) cudaFree(r->ctr);
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
@@ -2534,7 +2589,7 @@ int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has
   rc = ensure_scratch(r, (prog.nslots + 1) * cap * 4 * kWarpsPerBlock * blocks);
   if (rc) return rc;
   const uint64_t kSlotChunk = 1ull << 22;
-  unsigned long long *uval = nullptr, *uoff = nullptr, *dtot = nullptr;
+  unsigned long long *uval = nullptr, *uoff = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   SMG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, uval, uoff, kSlotChunk + 1, st));
@@ -2543,7 +2598,6 @@ int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has
   SMG_CUDA(cudaMalloc(&tmp, tmp_bytes));
   uint32_t* dout = nullptr;
   size_t dout_cap = 0;
-  (void)dtot;
   KernelArgs a;
   std::memset(&a, 0, sizeof(a));
   a.off = r.off;
