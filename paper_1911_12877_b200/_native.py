@@ -84,11 +84,6 @@ def gpu_lib():
     with _lock:
         if _gpu is None:
             path = _build.ensure_engine()
-            variant = os.environ.get("SMG_ENGINE_VARIANT")  # tuning experiments only
-            if variant:
-                path = path.replace(".so", f"_{variant}.so")
-                if not os.path.exists(path):
-                    raise IoError(f"engine variant {variant!r} not built: {path}")
             lib = ctypes.CDLL(path)
             _bind(lib, "smg_abi_version", ctypes.c_int, [])
             _bind(lib, "smg_last_error", ctypes.c_char_p, [])

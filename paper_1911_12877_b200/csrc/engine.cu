@@ -433,6 +433,41 @@ __device__ uint32_t filter_list(const Ctx& c, const uint32_t* X, uint32_t nX, co
   return written;
 }
 
+// The warp's global bitmap (Ctx::gbm) as a probe set: fill with arr[0..n),
+// probe with one L2 load, clear the touched words again.  Chosen over a
+// bisection probe by a latency model: fill ~n/16 + stream ~m/128 rounds vs
+// ~(k/32) * log2(len) dependent rounds of bisection.
+__device__ __forceinline__ void gbm_fill(const Ctx& c, const uint32_t* arr, uint32_t n) {
+  __syncwarp();
+  for (uint32_t i = c.lane; i < n; i += 32) {
+    const uint32_t x = arr[i];
+    atomicOr(c.gbm + (x >> 5), 1u << (x & 31));
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void gbm_clear(const Ctx& c, const uint32_t* arr, uint32_t n) {
+  __syncwarp();
+  for (uint32_t i = c.lane; i < n; i += 32) c.gbm[arr[i] >> 5] = 0u;
+  __syncwarp();
+}
+
+__device__ __forceinline__ bool gbm_better(uint32_t n_fill, uint32_t n_stream, uint32_t n_search,
+                                           uint32_t search_len) {
+  const uint32_t bm = (n_fill + 15) / 16 + (n_stream + 127) / 128;
+  const uint32_t bs = ((n_search + 31) / 32) * static_cast<uint32_t>(ilog2p1(search_len));
+  return bm < bs;
+}
+
+__device__ __forceinline__ ProbeSet gbm_probe(const Ctx& c) {
+  ProbeSet p;
+  p.arr = nullptr;
+  p.n = 0;
+  p.hash = c.gbm;
+  p.bits = -1;
+  return p;
+}
+
 // Apply a node's ops to the input set `in` (sorted, already bounded).
 // COUNT: return |result| only; else write the sorted result to `out`.
 template <bool COUNT>
@@ -458,6 +493,12 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
         const ProbeSet pr = make_probe(c, Sm, nSm, true);
         return filter_list<COUNT>(c, Lg, nLg, pr, true, kEmptySlot, out);
       }
+      if (c.gbm && 2 * nSm > kHashSlots && gbm_better(nSm, nLg, nSm, nLg)) {
+        gbm_fill(c, Sm, nSm);
+        const uint32_t r = filter_list<COUNT>(c, Lg, nLg, gbm_probe(c), true, kEmptySlot, out);
+        gbm_clear(c, Sm, nSm);
+        return r;
+      }
       const ProbeSet pr = make_probe(c, Lg, nLg, false);
       return filter_list<COUNT>(c, Sm, nSm, pr, true, kEmptySlot, out);
     }
@@ -473,6 +514,12 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
       return filter_list<COUNT>(c, in, inlen, none, false, v, out);
     }
     const bool hash = 2 * (b - a) <= kHashSlots && (b - a) <= 8u * inlen;
+    if (!hash && c.gbm && gbm_better(b - a, inlen, inlen, b - a)) {
+      gbm_fill(c, L + a, b - a);
+      const uint32_t r = filter_list<COUNT>(c, in, inlen, gbm_probe(c), false, v, out);
+      gbm_clear(c, L + a, b - a);
+      return r;
+    }
     const ProbeSet pr = make_probe(c, L + a, b - a, hash);
     return filter_list<COUNT>(c, in, inlen, pr, false, v, out);
   }
@@ -702,10 +749,7 @@ __device__ uint64_t stream_count(const Ctx& c, const uint32_t* S, uint32_t nS, c
       const uint32_t jlo = __shfl_sync(kFull, lo_val, j);
       const uint32_t jhi = __shfl_sync(kFull, hi_val, j);
       if (TRACE && c.lane == 0) tr[kTrStreamElems] += jl;  // upper bound (early exit)
-      if (c.tune & 8u)
-        hits += stream_long<8>(c, jp, jl, jlo, jhi, P, tr);
-      else
-        hits += stream_long<4>(c, jp, jl, jlo, jhi, P, tr);
+      hits += stream_long<kUnroll>(c, jp, jl, jlo, jhi, P, tr);
     }
     // 2) short lists: flattened over the lanes, range-filtered per element
     const uint32_t slen = is_long || search ? 0u : len;
@@ -1203,7 +1247,14 @@ __device__ uint64_t clique_local_warp(const Ctx& c, const Program& P, uint32_t* 
   return local_dfs<1>(c, P, rows, kLocalWarpRowWords, u, q0, q1, 0, 1);
 }
 
-template <bool METER, bool TRACE>
+// SHAPE: kShapeGeneric runs every path; kShapeBatch4 is the depth-4 plan
+// with a batched leaf (clique4, rectangle, every 4-vertex motif): the unit's
+// loop-0/1 sets, then one leaf batch -- the deeper-loop DFS, per-sibling
+// leaves and clique-local paths are compiled out, which keeps the hot code
+// small enough for the instruction caches at 64 resident warps per SM.
+enum { kShapeGeneric = 0, kShapeBatch4 = 1 };
+
+template <bool METER, bool TRACE, int SHAPE>
 __global__ void __launch_bounds__(kThreads, SMG_COUNT_MINB) count_kernel(const KernelArgs a) {
   __shared__ WarpState states[kWarpsPerBlock];
   extern __shared__ uint32_t dyn_smem[];
@@ -1275,6 +1326,13 @@ __global__ void __launch_bounds__(kThreads, SMG_COUNT_MINB) count_kernel(const K
       for (int t = P.node_begin[0]; t < P.node_end[0]; ++t) build_node(c, P, t);
       for (int t = P.node_begin[1]; t < P.node_end[1]; ++t) build_node(c, P, t);
       if (TRACE) tr[kTrBuildCycles] += clock64() - tclk;
+      if (SHAPE == kShapeBatch4) {
+        if (METER) elems += meter_batch(c, P);
+        if (TRACE) tclk = clock64();
+        checked_acc(cnt, leaf_batch<TRACE>(c, P, hq, tr), ovf);
+        if (TRACE) tr[kTrBatchCycles] += clock64() - tclk;
+        continue;
+      } else {
       if (P.depth == 3) {
         checked_acc(cnt, leaf_count(c, P), ovf);
         continue;
@@ -1338,6 +1396,7 @@ __global__ void __launch_bounds__(kThreads, SMG_COUNT_MINB) count_kernel(const K
           pos[level] = 0;
         }
       }
+      }  // SHAPE
     }
   }
   if (lane == 0) {
@@ -2079,14 +2138,14 @@ struct Launch {
 };
 
 // Enqueue one shard on replica r (asynchronous).  Caller holds r.mu.
-template <bool METER, bool TRACE>
+template <bool METER, bool TRACE, int SHAPE>
 int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
   const uint64_t cap = std::max<uint64_t>(32, (g.max_degree + 31) / 32 * 32);
   const bool heavy = prog.batch != 0;
-  SMG_CUDA(cudaFuncSetAttribute(count_kernel<METER, TRACE>,
+  SMG_CUDA(cudaFuncSetAttribute(count_kernel<METER, TRACE, SHAPE>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDynSmem)));
   int per_sm = 0;
-  SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_kernel<METER, TRACE>, kThreads,
+  SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_kernel<METER, TRACE, SHAPE>, kThreads,
                                                          kDynSmem));
   per_sm = std::max(1, per_sm);
   uint64_t blocks = static_cast<uint64_t>(r.num_sms) * per_sm;
@@ -2109,7 +2168,7 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
     }
   }
   const uint64_t bm_words = (g.n + 31) / 32;
-  if (prog.batch) {
+  {
     const size_t bytes = blocks * kWarpsPerBlock * bm_words * sizeof(uint32_t);
     if (r.warp_bitmaps_bytes < bytes) {
       if (r.warp_bitmaps) cudaFree(r.warp_bitmaps);
@@ -2167,12 +2226,12 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.heavy_cap = heavy ? kHeavyQueueCap : 0;
   a.heavy_scratch = r.heavy_scratch;
   a.local_rows = clique ? r.local_rows : nullptr;
-  a.warp_bitmaps = (prog.batch && !(g_tune & 64u)) ? r.warp_bitmaps : nullptr;
+  a.warp_bitmaps = !(g_tune & 64u) ? r.warp_bitmaps : nullptr;
   a.bitmap_words = bm_words;
   a.heavy_rows = clique ? r.heavy_rows : nullptr;
   a.prog = prog;
   if (L.unit_end > L.unit_begin) {
-    count_kernel<METER, TRACE><<<static_cast<unsigned>(blocks), kThreads, kDynSmem, st>>>(a);
+    count_kernel<METER, TRACE, SHAPE><<<static_cast<unsigned>(blocks), kThreads, kDynSmem, st>>>(a);
     if (heavy) {
       const size_t hsm = clique ? std::max(kHeavySmem, kBitmapWords * 4 + kHeavyCliqueSmem) : kHeavySmem;
       SMG_CUDA(cudaFuncSetAttribute(heavy_kernel<TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2191,8 +2250,18 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
 
 int enqueue(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
   SMG_CUDA(cudaSetDevice(r.device));
-  if (L.meter) return g_trace ? enqueue_t<true, true>(g, r, prog, L) : enqueue_t<true, false>(g, r, prog, L);
-  return g_trace ? enqueue_t<false, true>(g, r, prog, L) : enqueue_t<false, false>(g, r, prog, L);
+  if (prog.batch && prog.depth == 4) {
+    if (L.meter)
+      return g_trace ? enqueue_t<true, true, kShapeBatch4>(g, r, prog, L)
+                     : enqueue_t<true, false, kShapeBatch4>(g, r, prog, L);
+    return g_trace ? enqueue_t<false, true, kShapeBatch4>(g, r, prog, L)
+                   : enqueue_t<false, false, kShapeBatch4>(g, r, prog, L);
+  }
+  if (L.meter)
+    return g_trace ? enqueue_t<true, true, kShapeGeneric>(g, r, prog, L)
+                   : enqueue_t<true, false, kShapeGeneric>(g, r, prog, L);
+  return g_trace ? enqueue_t<false, true, kShapeGeneric>(g, r, prog, L)
+                 : enqueue_t<false, false, kShapeGeneric>(g, r, prog, L);
 }
 
 int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* ovf, double* ms) {
