@@ -7,6 +7,9 @@ cd "$(dirname "$0")/.."
 for cfg in $CFGS; do
   python -c "from paper_1911_12877_b200 import configs; configs.load('$cfg', verbose=True)" 2>&1 | tail -1
   for label in $(python -c "from paper_1911_12877_b200 import configs; print(' '.join(l for l,_ in configs.config_patterns('$cfg')))"); do
-    timeout $T python tools/probe_one.py $cfg $label 2>&1 | tail -3 || echo "$cfg $label: timeout/fail rc=$?"
+    timeout $T python tools/probe_one.py $cfg $label > /tmp/sweep_one.log 2>&1
+    rc=$?
+    tail -1 /tmp/sweep_one.log
+    [ $rc -ne 0 ] && echo "$cfg $label: not finished within ${T}s (rc=$rc)"
   done
 done
