@@ -39,16 +39,15 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr uint32_t kChunk = 32;  // edge slots per queue grab
 constexpr unsigned kFull = 0xffffffffu;
-#ifndef SMG_HASH_LOG2
-#define SMG_HASH_LOG2 9
-#endif
-#ifndef SMG_COUNT_MINB
-#define SMG_COUNT_MINB 8
-#endif
-constexpr int kHashLog2 = SMG_HASH_LOG2;  // per-warp shared-memory hash: 512 slots (2 KB)
-constexpr uint32_t kHashSlots = 1u << kHashLog2;
+// Per-warp shared-memory hash.  The generic kernel (plans of depth >= 5, the
+// clique-local path) keeps 2048 slots (8 KB) at 3 CTAs/SM; the depth-4 batch
+// kernel trades table size for residency: 512 slots (2 KB) at 8 CTAs/SM =
+// 64 warps/SM (measured: profiles/r01_tuning.md).
+constexpr uint32_t kHashSlots = 2048;       // generic shape (and the static maximum)
+constexpr uint32_t kBatchHashSlots = 512;   // depth-4 batch shape
 constexpr uint32_t kEmptySlot = 0xffffffffu;  // never a vertex id (ids < n < 2^32)
 constexpr size_t kDynSmem = sizeof(uint32_t) * kHashSlots * kWarpsPerBlock;
+constexpr size_t kBatchDynSmem = sizeof(uint32_t) * kBatchHashSlots * kWarpsPerBlock;
 // CTA tier (heavy_kernel): two 16-warp CTAs per SM (one can run while the
 // other waits at a barrier).  Node builds probe an 8K-slot (32 KB) hash
 // table; the batched leaf probes a 512K-bit (64 KB) bitmap of the probe set
@@ -65,7 +64,10 @@ constexpr int kHeavyThreads = kHeavyWarps * 32;
 #define SMG_HEAVY_MINB 2
 #endif
 constexpr int kHeavyMinBlocks = SMG_HEAVY_MINB;             // CTAs per SM
-constexpr uint32_t kHeavySlots = 1u << 13;
+#ifndef SMG_HEAVY_SLOTS_LOG2
+#define SMG_HEAVY_SLOTS_LOG2 13
+#endif
+constexpr uint32_t kHeavySlots = 1u << SMG_HEAVY_SLOTS_LOG2;
 constexpr uint32_t kBitmapWords = 1u << SMG_BITMAP_LOG2;    // 64 KB
 constexpr uint64_t kBitmapSpan = uint64_t(kBitmapWords) * 32;  // ids per slice
 constexpr size_t kHeavySmem = sizeof(uint32_t) * (kHeavySlots + kBitmapWords);
@@ -264,6 +266,7 @@ struct Ctx {
   uint32_t heavy_stream;  // defer batches streaming at least this many elements (0: off)
   uint32_t heavy_min;     // defer big-probe-set batches only above this streamed degree sum
   uint32_t* gbm;          // this warp's global bitmap over all ids (zero between uses), or null
+  uint32_t hslots;        // slots of `hash` (power of two)
 };
 
 __device__ __forceinline__ void nbrs(const Ctx& c, uint32_t v, const uint32_t*& p, uint32_t& len) {
@@ -364,7 +367,7 @@ __device__ __forceinline__ ProbeSet make_probe(const Ctx& c, const uint32_t* arr
   p.hi = arr[n - 1];
   p.hash = c.hash;
   p.bits = 0;
-  if (hash && 2 * n <= kHashSlots) {
+  if (hash && 2 * n <= c.hslots) {
     p.bits = table_bits(n);
     __syncwarp();
     fill_table(c.hash, p, c.lane, 32);
@@ -398,8 +401,8 @@ __device__ __forceinline__ int ilog2p1(uint32_t x) { return 32 - __clz(x | 1u); 
 // side into the large one?  Per-warp cycle model: a binary-search round costs
 // ~log2(large) dependent loads, a stream iteration ~one load latency per
 // 32*kUnroll elements.
-__device__ __forceinline__ bool prefer_stream(uint32_t small, uint32_t large) {
-  if (small * 2 > kHashSlots) return false;
+__device__ __forceinline__ bool prefer_stream(uint32_t small, uint32_t large, uint32_t hslots) {
+  if (small * 2 > hslots) return false;
   const uint64_t bs = static_cast<uint64_t>((small + 31) / 32) * ilog2p1(large);
   const uint64_t st = (large + 32 * kUnroll - 1) / (32 * kUnroll) + (small + 31) / 32;
   return st < bs;
@@ -462,7 +465,7 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
       const uint32_t nSm = in_small ? inlen : nL;
       const uint32_t* Lg = in_small ? L : in;
       const uint32_t nLg = in_small ? nL : inlen;
-      if (prefer_stream(nSm, nLg)) {
+      if (prefer_stream(nSm, nLg, c.hslots)) {
         X = Lg, nX = nLg, Q = Sm, nQ = nSm, use_hash = true;
       } else {
         X = Sm, nX = nSm, Q = Lg, nQ = nLg;  // bisection into the large side
@@ -476,7 +479,7 @@ __device__ uint32_t apply_ops(const Ctx& c, const Node& nd, const uint32_t* in, 
       const uint32_t wb = wa + warp_lower_bound<true>(L + wa, nL - wa, hi + 1u);
       Q = L + wa;
       nQ = wb - wa;
-      use_hash = nQ && 2 * nQ <= kHashSlots && nQ <= 8u * inlen;
+      use_hash = nQ && 2 * nQ <= c.hslots && nQ <= 8u * inlen;
     }
     // (A global-bitmap probe set for big node operands was measured slower
     // than bisection here: +4-7 % on cfg2; it stays on the leaf batches.)
@@ -915,8 +918,8 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
     ps.hi = ps.arr[ps.n - 1];
     ps.hash = c.hash;
     ps.bits = 0;
-    if (b.same && (ps.n * 2 > kHashSlots || c.heavy_stream)) sum_s = degree_sum(c, b.A, b.nA, 0, 32);
-    if (ps.n * 2 > kHashSlots || (c.heavy_stream && sum_s >= c.heavy_stream)) {
+    if (b.same && (ps.n * 2 > c.hslots || c.heavy_stream)) sum_s = degree_sum(c, b.A, b.nA, 0, 32);
+    if (ps.n * 2 > c.hslots || (c.heavy_stream && sum_s >= c.heavy_stream)) {
       // Too big for the warp's table (or a long stream).  Queue it for the CTA
       // tier unless the streaming side is trivially small (then binary search
       // is cheaper).
@@ -933,7 +936,7 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
       }
     }
     bool global_bm = false;
-    if (ps.n * 2 > kHashSlots && c.gbm) {
+    if (ps.n * 2 > c.hslots && c.gbm) {
       // Too big for the warp's smem table: a bitmap over all ids in global
       // memory (L2-resident words), one dependent load per probe instead of
       // a bisection chain; cleared again below.
@@ -946,7 +949,7 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
       ps.bits = -1;
       global_bm = true;
     }
-    if (ps.n * 2 <= kHashSlots) {
+    if (ps.n * 2 <= c.hslots) {
       ps.bits = table_bits(ps.n);
       __syncwarp();
       fill_table(c.hash, ps, c.lane, 32);
@@ -986,7 +989,7 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
 // the CTA tier (heavy_kernel) with |U| <= kLocalCtaMax; beyond that the
 // generic path runs.
 
-constexpr uint32_t kLocalWarpMax = kHashSlots / 4;  // keys, index and row buffer fit the warp hash area
+constexpr uint32_t kLocalWarpMax = kHashSlots / 4;  // keys, index and row buffer fit the generic warp hash area
 constexpr uint32_t kLocalCtaMax = 4096;
 constexpr uint32_t kLocalCtaSlots = 2 * kLocalCtaMax;            // index table slots
 constexpr uint32_t kLocalRowWords = kLocalCtaMax / 32;           // CTA row stride (words)
@@ -1222,7 +1225,7 @@ __device__ uint64_t clique_local_warp(const Ctx& c, const Program& P, uint32_t* 
 enum { kShapeGeneric = 0, kShapeBatch4 = 1 };
 
 template <bool METER, bool TRACE, int SHAPE>
-__global__ void __launch_bounds__(kThreads, SMG_COUNT_MINB) count_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(kThreads, SHAPE == kShapeBatch4 ? 8 : 3) count_kernel(const KernelArgs a) {
   __shared__ WarpState states[kWarpsPerBlock];
   extern __shared__ uint32_t dyn_smem[];
   const int lane = threadIdx.x & 31;
@@ -1241,7 +1244,8 @@ __global__ void __launch_bounds__(kThreads, SMG_COUNT_MINB) count_kernel(const K
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
-  c.hash = dyn_smem + wib * kHashSlots;
+  c.hslots = SHAPE == kShapeBatch4 ? kBatchHashSlots : kHashSlots;
+  c.hash = dyn_smem + wib * c.hslots;
   const bool batch = P.batch;
   HeavyQueue hq;
   hq.items = a.heavy_items;
@@ -1731,6 +1735,7 @@ __global__ void __launch_bounds__(kHeavyThreads, kHeavyMinBlocks) heavy_kernel(c
   c.heavy_stream = 0;
   c.heavy_min = 0;
   c.gbm = nullptr;
+  c.hslots = kHashSlots;
   c.hash = table;
   uint64_t trbuf[TRACE ? kTrCount : 1];
   if (TRACE)
@@ -1755,10 +1760,11 @@ __global__ void __launch_bounds__(kHeavyThreads, kHeavyMinBlocks) heavy_kernel(c
       const int un = clique_universe(sh.st, P);
       const uint32_t* U = sh.st.ptr[un];
       const uint32_t u = sh.st.len[un];
+      // the local index and row buffers borrow the (idle) bitmap region
       LocalIndex L;
-      L.keys = table;
-      L.idx = reinterpret_cast<uint16_t*>(table + kLocalCtaSlots);
-      uint32_t* rowbuf = table + kLocalCtaSlots + kLocalCtaSlots / 2 + warp * kLocalRowWords;
+      L.keys = bm;
+      L.idx = reinterpret_cast<uint16_t*>(bm + kLocalCtaSlots);
+      uint32_t* rowbuf = bm + kLocalCtaSlots + kLocalCtaSlots / 2 + warp * kLocalRowWords;
       local_index_build(L, U, u, threadIdx.x, kHeavyThreads, true);
       for (uint32_t w = lane; w < kLocalRowWords; w += 32) rowbuf[w] = 0u;
       __syncwarp();
@@ -1784,6 +1790,8 @@ __global__ void __launch_bounds__(kHeavyThreads, kHeavyMinBlocks) heavy_kernel(c
           tr[kTrHeavyCycles] += clock64() - t0;
         }
       }
+      for (uint32_t i = threadIdx.x; i < kBitmapWords / 4; i += kHeavyThreads)
+        table4[i] = make_uint4(0u, 0u, 0u, 0u);  // batch items expect a zero bitmap
       __syncthreads();
       continue;
     }
@@ -1917,6 +1925,7 @@ __global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
+  c.hslots = kHashSlots;
   c.hash = dyn_smem + wib * kHashSlots;
   uint32_t* leafbuf = c.scratch + static_cast<uint64_t>(P.nslots) * a.cap;
   WarpState& s = states[wib];
@@ -2121,11 +2130,12 @@ template <bool METER, bool TRACE, int SHAPE>
 int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
   const uint64_t cap = std::max<uint64_t>(32, (g.max_degree + 31) / 32 * 32);
   const bool heavy = prog.batch != 0;
+  const size_t dyn = SHAPE == kShapeBatch4 ? kBatchDynSmem : kDynSmem;
   SMG_CUDA(cudaFuncSetAttribute(count_kernel<METER, TRACE, SHAPE>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDynSmem)));
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
   int per_sm = 0;
   SMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_kernel<METER, TRACE, SHAPE>, kThreads,
-                                                         kDynSmem));
+                                                         dyn));
   per_sm = std::max(1, per_sm);
   uint64_t blocks = static_cast<uint64_t>(r.num_sms) * per_sm;
   // Keep the per-warp scratch within a budget (sets are at most max_degree).
@@ -2210,9 +2220,10 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.heavy_rows = clique ? r.heavy_rows : nullptr;
   a.prog = prog;
   if (L.unit_end > L.unit_begin) {
-    count_kernel<METER, TRACE, SHAPE><<<static_cast<unsigned>(blocks), kThreads, kDynSmem, st>>>(a);
+    count_kernel<METER, TRACE, SHAPE><<<static_cast<unsigned>(blocks), kThreads, dyn, st>>>(a);
     if (heavy) {
-      const size_t hsm = clique ? std::max(kHeavySmem, kBitmapWords * 4 + kHeavyCliqueSmem) : kHeavySmem;
+      static_assert(kHeavyCliqueSmem <= kBitmapWords * 4, "clique-local region must fit the bitmap region");
+      const size_t hsm = kHeavySmem;
       SMG_CUDA(cudaFuncSetAttribute(heavy_kernel<TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hsm)));
       int hper = 0;
