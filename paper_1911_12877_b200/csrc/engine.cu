@@ -71,7 +71,7 @@ constexpr uint32_t kHeavySlots = 1u << SMG_HEAVY_SLOTS_LOG2;
 constexpr uint32_t kBitmapWords = 1u << SMG_BITMAP_LOG2;    // 64 KB
 constexpr uint64_t kBitmapSpan = uint64_t(kBitmapWords) * 32;  // ids per slice
 constexpr size_t kHeavySmem = sizeof(uint32_t) * (kHeavySlots + kBitmapWords);
-constexpr uint64_t kHeavyMinStream = 65536;  // defer only batches with real streaming work
+constexpr uint64_t kHeavyMinStream = 32768;  // defer only batches with real streaming work
 constexpr uint64_t kHeavyQueueCap = 1ull << 24;
 
 // ---------------------------------------------------------------- device ---
@@ -1539,10 +1539,13 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
       }
     }
   }
-  // two passes over per-warp slices: count, scan, write in order
+  // One filter pass over per-warp slices, each compacted into the staging
+  // slot at its own input offset; after a scan of the slice counts every warp
+  // copies its run to the final position (no second probe pass).
+  uint32_t* stage = c.scratch + static_cast<uint64_t>(P.nslots) * c.cap;
   const uint32_t chunk = ((nX + kHeavyWarps - 1) / kHeavyWarps + 255) / 256 * 256;
   const uint32_t lo = min(nX, warp * chunk), hi = min(nX, lo + chunk);
-  const uint32_t cnt = filter_list<true, 8>(c, X + lo, hi - lo, pr, keep_found, exclude, nullptr);
+  const uint32_t cnt = filter_list<false, 8>(c, X + lo, hi - lo, pr, keep_found, exclude, stage + lo);
   if (lane == 0) sh.wsum[warp] = cnt;
   __syncthreads();
   uint32_t off = 0, total = 0;
@@ -1550,7 +1553,7 @@ __device__ void cta_build_node(const Ctx& c, const Program& P, int t, HeavyShare
     off += w < warp ? sh.wsum[w] : 0u;
     total += sh.wsum[w];
   }
-  filter_list<false, 8>(c, X + lo, hi - lo, pr, keep_found, exclude, out + off);
+  for (uint32_t i = lane; i < cnt; i += 32) out[off + i] = stage[lo + i];
   __syncthreads();
   if (threadIdx.x == 0) {
     sh.st.ptr[t] = out;
@@ -1727,7 +1730,7 @@ __global__ void __launch_bounds__(kHeavyThreads, kHeavyMinBlocks) heavy_kernel(c
   c.off = a.off;
   c.adj = a.adj;
   c.s = &sh.st;
-  c.scratch = a.heavy_scratch + static_cast<uint64_t>(blockIdx.x) * P.nslots * a.cap;
+  c.scratch = a.heavy_scratch + static_cast<uint64_t>(blockIdx.x) * (P.nslots + 1) * a.cap;  // + staging slot
   c.cap = a.cap;
   c.lane = lane;
   c.nv = static_cast<float>(a.nverts);
@@ -2106,6 +2109,82 @@ struct smg_graph {
 
 namespace smg {
 
+// Work buffers (per-warp scratch, the CTA-tier queue and scratch, the warp
+// bitmaps, clique-local rows) are sized by the launch, not by the graph, so a
+// destroyed replica parks them per device and the next replica on that device
+// adopts them: a new smg_graph (e.g. one per call through the C++ adapter or
+// the e2e bench path) does not pay gigabytes of cudaMalloc/cudaFree + memset.
+// The bitmaps are all-zero whenever no kernel runs, so they can be reused.
+struct WorkSet {
+  uint32_t* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  uint32_t* heavy_items = nullptr;
+  uint32_t* heavy_scratch = nullptr;
+  size_t heavy_scratch_bytes = 0;
+  uint32_t* local_rows = nullptr;
+  size_t local_rows_bytes = 0;
+  uint32_t* warp_bitmaps = nullptr;
+  size_t warp_bitmaps_bytes = 0;
+  uint32_t* heavy_rows = nullptr;
+  size_t heavy_rows_bytes = 0;
+};
+std::mutex g_pool_mu;
+WorkSet g_pool[64];  // one parked set per device ordinal
+bool g_pool_used[64] = {};
+
+void free_work(WorkSet& w) {
+  if (w.scratch) cudaFree(w.scratch);
+  if (w.heavy_items) cudaFree(w.heavy_items);
+  if (w.heavy_scratch) cudaFree(w.heavy_scratch);
+  if (w.local_rows) cudaFree(w.local_rows);
+  if (w.warp_bitmaps) cudaFree(w.warp_bitmaps);
+  if (w.heavy_rows) cudaFree(w.heavy_rows);
+  w = WorkSet();
+}
+
+void park_work(Replica& r) {
+  WorkSet w;
+  w.scratch = r.scratch;
+  w.scratch_bytes = r.scratch_bytes;
+  w.heavy_items = r.heavy_items;
+  w.heavy_scratch = r.heavy_scratch;
+  w.heavy_scratch_bytes = r.heavy_scratch_bytes;
+  w.local_rows = r.local_rows;
+  w.local_rows_bytes = r.local_rows_bytes;
+  w.warp_bitmaps = r.warp_bitmaps;
+  w.warp_bitmaps_bytes = r.warp_bitmaps_bytes;
+  w.heavy_rows = r.heavy_rows;
+  w.heavy_rows_bytes = r.heavy_rows_bytes;
+  if (r.device < 0 || r.device >= 64) {
+    free_work(w);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (g_pool_used[r.device]) free_work(g_pool[r.device]);  // keep the newest set
+  g_pool[r.device] = w;
+  g_pool_used[r.device] = true;
+}
+
+void adopt_work(Replica& r) {
+  if (r.device < 0 || r.device >= 64) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool_used[r.device]) return;
+  WorkSet& w = g_pool[r.device];
+  r.scratch = w.scratch;
+  r.scratch_bytes = w.scratch_bytes;
+  r.heavy_items = w.heavy_items;
+  r.heavy_scratch = w.heavy_scratch;
+  r.heavy_scratch_bytes = w.heavy_scratch_bytes;
+  r.local_rows = w.local_rows;
+  r.local_rows_bytes = w.local_rows_bytes;
+  r.warp_bitmaps = w.warp_bitmaps;
+  r.warp_bitmaps_bytes = w.warp_bitmaps_bytes;
+  r.heavy_rows = w.heavy_rows;
+  r.heavy_rows_bytes = w.heavy_rows_bytes;
+  w = WorkSet();
+  g_pool_used[r.device] = false;
+}
+
 int ensure_scratch(Replica& r, size_t bytes) {
   if (r.scratch_bytes >= bytes) return SMG_OK;
   if (r.scratch) cudaFree(r.scratch);
@@ -2147,7 +2226,7 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   if (heavy) {
     if (!r.heavy_items)
       SMG_CUDA(cudaMalloc(&r.heavy_items, kHeavyQueueCap * kHeavyItemWords * sizeof(uint32_t)));
-    const size_t hs = static_cast<size_t>(r.num_sms) * 4 * prog.nslots * cap * 4;  // <= 4 CTAs/SM
+    const size_t hs = static_cast<size_t>(r.num_sms) * 4 * (prog.nslots + 1) * cap * 4;  // <= 4 CTAs/SM
     if (r.heavy_scratch_bytes < hs) {
       if (r.heavy_scratch) cudaFree(r.heavy_scratch);
       r.heavy_scratch = nullptr;
@@ -2359,12 +2438,7 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->off) cudaFree(r->off);
     if (r->adj) cudaFree(r->adj);
     if (r->src) cudaFree(r->src);
-    if (r->scratch) cudaFree(r->scratch);
-    if (r->heavy_items) cudaFree(r->heavy_items);
-    if (r->heavy_scratch) cudaFree(r->heavy_scratch);
-    if (r->local_rows) cudaFree(r->local_rows);
-    if (r->warp_bitmaps) cudaFree(r->warp_bitmaps);
-    if (r->heavy_rows) cudaFree(r->heavy_rows);
+    park_work(*r);  // per-warp scratch, queues and bitmaps go to the device's pool
     if (r->ctr) cudaFree(r->ctr);
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
     if (r->ev0) cudaEventDestroy(r->ev0);
@@ -2414,6 +2488,7 @@ int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_
     Replica* r = new Replica;
     g->reps.push_back(r);
     r->device = dev;
+    adopt_work(*r);
     auto step = [&](cudaError_t e, const char* what) {
       if (e != cudaSuccess) {
         g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
@@ -2450,6 +2525,7 @@ int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_
 // Runtime parts of a replica (stream, events, counters) on `dev`.
 static int init_replica_runtime(Replica* r, int dev) {
   r->device = dev;
+  adopt_work(*r);
   SMG_CUDA(cudaSetDevice(dev));
   SMG_CUDA(cudaDeviceGetAttribute(&r->num_sms, cudaDevAttrMultiProcessorCount, dev));
   SMG_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
