@@ -266,6 +266,7 @@ struct Ctx {
   uint32_t heavy_stream;  // defer batches streaming at least this many elements (0: off)
   uint32_t heavy_min;     // defer big-probe-set batches only above this streamed degree sum
   uint32_t* gbm;          // this warp's global bitmap over all ids (zero between uses), or null
+  uint32_t gbm_words;     // its size in words
   uint32_t hslots;        // slots of `hash` (power of two)
 };
 
@@ -307,8 +308,20 @@ __device__ __forceinline__ uint32_t hbucket(uint32_t x, int bbits) {
 }
 
 __device__ __forceinline__ bool probe(const ProbeSet& P, uint32_t y) {
-  if (P.bits < 0)  // the warp's global (L2-resident) bitmap; L1 bypassed, it is rewritten per batch
-    return (__ldcg(P.hash + (y >> 5)) >> (y & 31)) & 1u;
+  if (P.bits < 0) {
+    if (P.bits == -1)  // the warp's global (L2-resident) bitmap; L1 bypassed, it is rewritten per batch
+      return (__ldcg(P.hash + (y >> 5)) >> (y & 31)) & 1u;
+    // radix index over the sorted P (see leaf_batch)
+    if (y < P.lo || y > P.hi) return false;
+    const uint32_t b = (y - P.lo) >> P.bm_base;
+    uint32_t i = __ldcg(P.hash + b);
+    const uint32_t e = __ldcg(P.hash + b + 1);
+    for (; i < e; ++i) {
+      const uint32_t v = P.arr[i];
+      if (v >= y) return v == y;
+    }
+    return false;
+  }
   if (P.bits) {
     const int bbits = P.bits - 2;
     const uint32_t mask = (1u << bbits) - 1u;
@@ -936,7 +949,34 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
       }
     }
     bool global_bm = false;
-    if (ps.n * 2 > c.hslots && c.gbm) {
+    uint32_t radix_nb = 0;
+    if (ps.n * 2 > c.hslots && c.gbm && (c.tune & 512u)) {
+      // Radix index over the sorted P (tune 512): bucket b of width 2^k holds
+      // P's positions [idx[b], idx[b+1]); ~2 elements per bucket, built in
+      // one pass without atomics; ~6 bytes per element of P in L2 instead of
+      // a 32-byte bitmap sector per element.
+      const uint32_t span = ps.hi - ps.lo;
+      int k = 0;
+      while ((static_cast<uint64_t>(span >> k) + 2) * 2 > ps.n && (span >> k) > 0) ++k;
+      radix_nb = (span >> k) + 2;
+      if (radix_nb <= c.gbm_words) {
+        uint32_t* idx = c.gbm;
+        for (uint32_t i = c.lane; i < ps.n; i += 32) {
+          const uint32_t bi = (ps.arr[i] - ps.lo) >> k;
+          const uint32_t bp = i ? ((ps.arr[i - 1] - ps.lo) >> k) + 1 : 0u;
+          for (uint32_t bb = bp; bb <= bi; ++bb) idx[bb] = i;
+          if (i == ps.n - 1)
+            for (uint32_t bb = bi + 1; bb < radix_nb; ++bb) idx[bb] = ps.n;
+        }
+        __syncwarp();
+        ps.hash = idx;
+        ps.bm_base = static_cast<uint32_t>(k);
+        ps.bits = -3;
+      } else {
+        radix_nb = 0;
+      }
+    }
+    if (ps.n * 2 > c.hslots && c.gbm && !radix_nb) {
       // Too big for the warp's smem table: a bitmap over all ids in global
       // memory (L2-resident words), one dependent load per probe instead of
       // a bisection chain; cleared again below.
@@ -969,6 +1009,11 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
     if (global_bm) {
       __syncwarp();
       for (uint32_t i = c.lane; i < ps.n; i += 32) c.gbm[ps.arr[i] >> 5] = 0u;
+      __syncwarp();
+    }
+    if (radix_nb) {
+      __syncwarp();
+      for (uint32_t i = c.lane; i < radix_nb; i += 32) c.gbm[i] = 0u;
       __syncwarp();
     }
     if (TRACE && !ps.bits) tr[kTrBigPCycles] += clock64() - t0;
@@ -1244,6 +1289,7 @@ __global__ void __launch_bounds__(kThreads, SHAPE == kShapeBatch4 ? 8 : 3) count
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
+  c.gbm_words = static_cast<uint32_t>(a.bitmap_words);
   c.hslots = SHAPE == kShapeBatch4 ? kBatchHashSlots : kHashSlots;
   c.hash = dyn_smem + wib * c.hslots;
   const bool batch = P.batch;
@@ -1928,6 +1974,7 @@ __global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
+  c.gbm_words = static_cast<uint32_t>(a.bitmap_words);
   c.hslots = kHashSlots;
   c.hash = dyn_smem + wib * kHashSlots;
   uint32_t* leafbuf = c.scratch + static_cast<uint64_t>(P.nslots) * a.cap;
