@@ -950,8 +950,9 @@ __device__ uint64_t leaf_batch(const Ctx& c, const Program& P, const HeavyQueue&
     }
     bool global_bm = false;
     uint32_t radix_nb = 0;
-    if (ps.n * 2 > c.hslots && c.gbm && (c.tune & 512u)) {
-      // Radix index over the sorted P (tune 512): bucket b of width 2^k holds
+    if (ps.n * 2 > c.hslots && c.gbm && !(c.tune & 512u)) {
+      // Radix index over the sorted P (SMG_TUNE 512: a plain bitmap instead):
+      // bucket b of width 2^k holds
       // P's positions [idx[b], idx[b+1]); ~2 elements per bucket, built in
       // one pass without atomics; ~6 bytes per element of P in L2 instead of
       // a 32-byte bitmap sector per element.
@@ -1461,6 +1462,7 @@ struct HeavyShared {
   uint32_t llo[kTile], lhi[kTile];
   uint32_t search_idx[kTile];
   uint32_t nsearch;
+  uint32_t chunk_next;  // cta_stream: next long-list chunk to claim
   uint32_t coffs[kTile + 1];  // long-list chunk offsets (cta_stream)
   uint32_t llen[kTile];        // long-list lengths (cta_stream)
 };
@@ -1632,7 +1634,10 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
   uint64_t hits = 0;
   for (uint32_t tile = 0; tile < nS; tile += kTile) {
     const uint32_t i = tile + threadIdx.x;
-    if (threadIdx.x == 0) sh.nsearch = 0;
+    if (threadIdx.x == 0) {
+      sh.nsearch = 0;
+      sh.chunk_next = 0;
+    }
     uint32_t len = 0, start = 0, lo_val = P.lo, hi_val = P.hi + 1u;
     const uint32_t* base = c.adj;
     if (i < nS) {
@@ -1683,31 +1688,7 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
       tr[kTrHeavyElems] += total;
       tr[kTrHeavyTiles] += 1;
     }
-    // 1) long lists, one warp per chunk
-    for (uint32_t q = warp; q < tch; q += kHeavyWarps) {
-      uint32_t j = 0;
-#pragma unroll
-      for (uint32_t step = kTile / 2; step >= 1; step >>= 1)
-        if (sh.coffs[j + step] <= q) j += step;
-      const uint32_t* lp = sh.lptr[j];
-      const uint32_t ll = sh.llen[j], jlo = sh.llo[j], jhi = sh.lhi[j];
-      const uint32_t e0 = (q - sh.coffs[j]) * kCtaChunk;
-      const uint32_t e1 = min(ll, e0 + kCtaChunk);
-      if (TRACE && lane == 0) tr[kTrStreamElems] += e1 - e0;
-      constexpr int kU = 8;  // loads in flight per lane
-      for (uint32_t t = e0 + lane; t < e1; t += 32 * kU) {
-        uint32_t y[kU];
-#pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          const uint32_t idx = t + 32 * k;
-          y[k] = idx < e1 ? __ldg(lp + idx) : kEmptySlot;
-        }
-#pragma unroll
-        for (int k = 0; k < kU; ++k)
-          if (y[k] >= jlo && y[k] < jhi && probe_bitmap(P, y[k])) ++hits;
-      }
-    }
-    // 2) short lists: load-balanced runs
+    // 1) short lists: load-balanced runs
     for (uint32_t e0 = threadIdx.x * kLbsRun; e0 < total; e0 += kTile * kLbsRun) {
       // owner of e0: the last j with offs[j] <= e0; its list state is kept in
       // registers and reloaded only when the run crosses into the next list
@@ -1741,6 +1722,35 @@ __device__ uint64_t cta_stream(const Ctx& c, const uint32_t* S, uint32_t nS, con
 #pragma unroll
       for (int k = 0; k < kLbsRun; ++k)
         if (y[k] >= ylo[k] && y[k] < yhi[k] && probe_bitmap(P, y[k])) ++hits;
+    }
+    // 2) long lists: whole warps claim chunks dynamically (after their share
+    //    of the short-list runs, so the tile ends balanced)
+    for (;;) {
+      uint32_t q = 0;
+      if (lane == 0) q = atomicAdd(&sh.chunk_next, 1u);
+      q = __shfl_sync(kFull, q, 0);
+      if (q >= tch) break;
+      uint32_t j = 0;
+#pragma unroll
+      for (uint32_t step = kTile / 2; step >= 1; step >>= 1)
+        if (sh.coffs[j + step] <= q) j += step;
+      const uint32_t* lp = sh.lptr[j];
+      const uint32_t ll = sh.llen[j], jlo = sh.llo[j], jhi = sh.lhi[j];
+      const uint32_t e0 = (q - sh.coffs[j]) * kCtaChunk;
+      const uint32_t e1 = min(ll, e0 + kCtaChunk);
+      if (TRACE && lane == 0) tr[kTrStreamElems] += e1 - e0;
+      constexpr int kU = 8;  // loads in flight per lane
+      for (uint32_t t = e0 + lane; t < e1; t += 32 * kU) {
+        uint32_t y[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          const uint32_t idx = t + 32 * k;
+          y[k] = idx < e1 ? __ldg(lp + idx) : kEmptySlot;
+        }
+#pragma unroll
+        for (int k = 0; k < kU; ++k)
+          if (y[k] >= jlo && y[k] < jhi && probe_bitmap(P, y[k])) ++hits;
+      }
     }
     // 3) skewed pairs: one warp per list, P's window binary-searched into N(s)
     for (uint32_t q = warp; q < sh.nsearch; q += kHeavyWarps) {
