@@ -104,7 +104,11 @@ struct KernelArgs {
   uint64_t cap;                   // scratch elements per slot
   uint64_t unit_begin, unit_end;  // edge-slot range
   uint64_t nverts;
-  uint32_t tune;  // SMG_TUNE bits (experiments): 1 = degree-only side choice, 2 = no clique-local
+  // SMG_TUNE bits (A/B switches kept for measurement; 0 = the tuned defaults):
+  //   1 degree-only side choice, 2 no clique-local, 16 always bisect long-list
+  //   windows, 64 no per-warp global work area (bisection probes for big P),
+  //   512 per-warp global bitmap instead of the radix index for big P
+  uint32_t tune;
   uint32_t heavy_stream;  // SMG_HEAVY_STREAM: CTA-tier threshold on a batch's streamed elements
   uint32_t heavy_min;     // SMG_HEAVY_MIN: big-probe-set batches stream at least this to be deferred
   uint32_t shard, num_shards;
