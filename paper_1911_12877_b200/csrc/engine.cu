@@ -1452,7 +1452,10 @@ __global__ void __launch_bounds__(kThreads, SHAPE == kShapeBatch4 ? 8 : 3) count
 // the table are split into value-range chunks (the streamed lists are
 // range-restricted per chunk, so every element is still probed exactly once).
 
-constexpr int kLbsRun = 8;
+#ifndef SMG_LBS_RUN
+#define SMG_LBS_RUN 8
+#endif
+constexpr int kLbsRun = SMG_LBS_RUN;
 constexpr int kTile = kHeavyThreads;
 
 struct HeavyShared {
@@ -1621,8 +1624,14 @@ __device__ __forceinline__ bool probe_bitmap(const ProbeSet& P, uint32_t y) {
   return (P.bm[d >> 5] >> (d & 31)) & 1u;
 }
 
-constexpr uint32_t kCtaLong = 256;          // lists this long are streamed in warp chunks
-constexpr uint32_t kCtaChunk = 1024;  // elements per warp chunk (4 rounds of 8 coalesced loads)
+#ifndef SMG_CTA_LONG
+#define SMG_CTA_LONG 256
+#endif
+#ifndef SMG_CTA_CHUNK
+#define SMG_CTA_CHUNK 1024
+#endif
+constexpr uint32_t kCtaLong = SMG_CTA_LONG;    // lists this long are streamed in warp chunks
+constexpr uint32_t kCtaChunk = SMG_CTA_CHUNK;  // elements per warp chunk (rounds of 8 coalesced loads)
 
 // CTA-wide stream: sum_{s in S} |N(s) & [lo_s, hi_s) & P| with P a bitmap.
 // Per tile of kTile lists every thread resolves one list's window (prefix

@@ -296,3 +296,55 @@ def test_batchable_plans():
         assert describe(rec["plan"])["batch"] == 1, rec["name"]
     # leaf with a single intersect source (the last level): not batched
     assert describe(named_plan("path", 4))["batch"] == 0
+
+
+def _radix_model(P, words):
+    """Python restatement of leaf_batch's radix index (engine.cu): buckets of
+    width 2^k over [P[0], P[-1]], ~2 elements each; idx[b] = first position
+    whose bucket >= b; a probe scans [idx[b], idx[b+1])."""
+    lo, hi, n = P[0], P[-1], len(P)
+    span = hi - lo
+    k = 0
+    while ((span >> k) + 2) * 2 > n and (span >> k) > 0:
+        k += 1
+    nb = (span >> k) + 2
+    if nb > words:
+        return None
+    idx = [None] * nb
+    for i in range(n):  # the lanes' writes are disjoint; order does not matter
+        bi = (P[i] - lo) >> k
+        bp = ((P[i - 1] - lo) >> k) + 1 if i else 0
+        for bb in range(bp, bi + 1):
+            idx[bb] = i
+        if i == n - 1:
+            for bb in range(bi + 1, nb):
+                idx[bb] = n
+    assert all(x is not None for x in idx)
+
+    def probe(y):
+        if y < lo or y > hi:
+            return False
+        b = (y - lo) >> k
+        for i in range(idx[b], idx[b + 1]):
+            if P[i] >= y:
+                return P[i] == y
+        return False
+    return probe
+
+
+def test_radix_index_model_matches_membership():
+    rng = np.random.default_rng(7)
+    for trial in range(60):
+        n = int(rng.integers(257, 3000))
+        universe = int(rng.choice([n + 5, 4 * n, 1 << 20, 1 << 31]))
+        P = np.unique(rng.integers(0, universe, size=n, dtype=np.int64)).tolist()
+        if len(P) < 2:
+            continue
+        probe = _radix_model(P, words=1 << 20)
+        assert probe is not None
+        Ps = set(P)
+        queries = rng.integers(0, universe, size=2000).tolist() + P[:50] + [P[0] - 1, P[-1] + 1]
+        for y in queries:
+            if y < 0:
+                continue
+            assert probe(y) == (y in Ps), (trial, y)
