@@ -107,7 +107,8 @@ struct KernelArgs {
   // SMG_TUNE bits (A/B switches kept for measurement; 0 = the tuned defaults):
   //   1 degree-only side choice, 2 no clique-local, 16 always bisect long-list
   //   windows, 64 no per-warp global work area (bisection probes for big P),
-  //   512 per-warp global bitmap instead of the radix index for big P
+  //   512 per-warp global bitmap instead of the radix index for big P,
+  //   1024 hub-hub units deferred before their loop-1 sets are built
   uint32_t tune;
   uint32_t heavy_stream;  // SMG_HEAVY_STREAM: CTA-tier threshold on a batch's streamed elements
   uint32_t heavy_min;     // SMG_HEAVY_MIN: big-probe-set batches stream at least this to be deferred
@@ -1344,6 +1345,22 @@ __global__ void __launch_bounds__(kThreads, SHAPE == kShapeBatch4 ? 8 : 3) count
       }
       __syncwarp();
       if (METER) elems += meter_level(c, P, 2);
+      if (SHAPE == kShapeBatch4 && !METER && (a.tune & 1024u) && hq.items) {
+        // (tune 1024) hub-hub units go straight to the CTA tier: their loop-1
+        // sets would be rebuilt there anyway
+        const uint32_t d0 = static_cast<uint32_t>(__ldg(c.off + v0 + 1) - __ldg(c.off + v0));
+        const uint32_t d1 = static_cast<uint32_t>(__ldg(c.off + v1 + 1) - __ldg(c.off + v1));
+        if (min(d0, d1) >= 2048u) {
+          unsigned long long slot = 0;
+          if (lane == 0) slot = atomicAdd(hq.count, 1ull);
+          slot = __shfl_sync(kFull, slot, 0);
+          if (slot < hq.cap) {
+            if (lane < 2) hq.items[slot * kHeavyItemWords + lane] = lane ? v1 : v0;
+            else if (lane == kHeavyItemWords - 1) hq.items[slot * kHeavyItemWords + lane] = 0u;
+            continue;
+          }
+        }
+      }
       if (TRACE) tclk = clock64();
       for (int t = P.node_begin[0]; t < P.node_end[0]; ++t) build_node(c, P, t);
       for (int t = P.node_begin[1]; t < P.node_end[1]; ++t) build_node(c, P, t);
