@@ -1888,6 +1888,11 @@ __global__ void __launch_bounds__(kHeavyThreads, kHeavyMinBlocks) heavy_kernel(c
     long long t1 = TRACE ? clock64() : 0;
     if (TRACE && threadIdx.x == 0) tr[kTrHeavyBuild] += t1 - t0;
     const BatchSets b = batch_sets(sh.st, P);
+    if (b.nA == 0 || b.nB == 0) {  // no leaf pairs (only early-deferred units can get here)
+      if (threadIdx.x == 0 && TRACE) tr[kTrHeavyItems] += 1;
+      __syncthreads();
+      continue;
+    }
     // side choice from the degree sums (CTA-wide)
     bool flip = false;
     if (!b.same) {
