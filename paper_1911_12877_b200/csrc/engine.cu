@@ -112,6 +112,7 @@ struct KernelArgs {
   uint32_t tune;
   uint32_t heavy_stream;  // SMG_HEAVY_STREAM: CTA-tier threshold on a batch's streamed elements
   uint32_t heavy_min;     // SMG_HEAVY_MIN: big-probe-set batches stream at least this to be deferred
+  float list_cost;        // SMG_LIST_COST
   uint32_t shard, num_shards;
   Counters* ctr;
   uint32_t* heavy_items;          // CTA-tier queue (kHeavyItemWords per item), may be null
@@ -273,6 +274,7 @@ struct Ctx {
   uint32_t* gbm;          // this warp's global bitmap over all ids (zero between uses), or null
   uint32_t gbm_words;     // its size in words
   uint32_t hslots;        // slots of `hash` (power of two)
+  float list_cost;        // per-list setup cost of a stream, in elements (side choice)
 };
 
 __device__ __forceinline__ void nbrs(const Ctx& c, uint32_t v, const uint32_t*& p, uint32_t& len) {
@@ -862,14 +864,14 @@ __device__ uint64_t diff_terms(const Ctx& c, const Program& P, const BatchSets& 
 // spreads roughly uniformly over the id range).
 // Each streamed list also pays a fixed setup (offsets, window search, a
 // warp-serial pass for long lists), ~kListCost elements' worth.
-constexpr float kListCost = 48.f;
+constexpr float kListCost = 384.f;  // default of Ctx::list_cost (SMG_LIST_COST); measured 16..4096
 __device__ __forceinline__ bool stream_b_cheaper(const Ctx& c, const BatchSets& b, uint64_t deg_a,
                                                  uint64_t deg_b) {
   if (c.tune & 1u) return deg_b < deg_a;
   const float wa = fminf(1.f, (static_cast<float>(b.A[b.nA - 1] - b.A[0]) + 1.f) / c.nv);
   const float wb = fminf(1.f, (static_cast<float>(b.B[b.nB - 1] - b.B[0]) + 1.f) / c.nv);
-  const float cost_a = kListCost * b.nA + static_cast<float>(deg_a) * wb;  // stream A's lists
-  const float cost_b = kListCost * b.nB + static_cast<float>(deg_b) * wa;
+  const float cost_a = c.list_cost * b.nA + static_cast<float>(deg_a) * wb;  // stream A's lists
+  const float cost_b = c.list_cost * b.nB + static_cast<float>(deg_b) * wa;
   return cost_b < cost_a;
 }
 
@@ -891,8 +893,8 @@ __device__ __forceinline__ bool choose_stream_b(const Ctx& c, const BatchSets& b
     const float wa = fminf(1.f, (static_cast<float>(b.A[b.nA - 1] - b.A[0]) + 1.f) / c.nv);
     const float wb = fminf(1.f, (static_cast<float>(b.B[b.nB - 1] - b.B[0]) + 1.f) / c.nv);
     const float wx = a_small ? wb : wa, wy = a_small ? wa : wb;  // window the other side clips to
-    const float cost_x = kListCost * nX + static_cast<float>(dx) * wx;
-    const float cost_y_min = (kListCost + wy) * nY;
+    const float cost_x = c.list_cost * nX + static_cast<float>(dx) * wx;
+    const float cost_y_min = (c.list_cost + wy) * nY;
     if (cost_y_min >= cost_x) {
       sum_s = dx;
       return !a_small;
@@ -1292,6 +1294,7 @@ __global__ void __launch_bounds__(kThreads, SHAPE == kShapeBatch4 ? 8 : 3) count
   c.lane = lane;
   c.nv = static_cast<float>(a.nverts);
   c.tune = a.tune;
+  c.list_cost = a.list_cost;
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
@@ -1821,6 +1824,7 @@ __global__ void __launch_bounds__(kHeavyThreads, kHeavyMinBlocks) heavy_kernel(c
   c.lane = lane;
   c.nv = static_cast<float>(a.nverts);
   c.tune = a.tune;
+  c.list_cost = a.list_cost;
   c.heavy_stream = 0;
   c.heavy_min = 0;
   c.gbm = nullptr;
@@ -2016,6 +2020,7 @@ __global__ void __launch_bounds__(kThreads) enum_kernel(const KernelArgs a, uint
   c.lane = lane;
   c.nv = static_cast<float>(a.nverts);
   c.tune = a.tune;
+  c.list_cost = a.list_cost;
   c.heavy_stream = a.heavy_stream;
   c.heavy_min = a.heavy_min;
   c.gbm = a.warp_bitmaps ? a.warp_bitmaps + gw * a.bitmap_words : nullptr;
@@ -2146,6 +2151,10 @@ const uint32_t g_heavy_stream = [] {
 const uint32_t g_heavy_min = [] {
   const char* e = std::getenv("SMG_HEAVY_MIN");
   return e ? static_cast<uint32_t>(std::atol(e)) : static_cast<uint32_t>(kHeavyMinStream);
+}();
+const float g_list_cost = [] {
+  const char* e = std::getenv("SMG_LIST_COST");
+  return e ? static_cast<float>(std::atof(e)) : kListCost;
 }();
 const int g_trace = [] {
   const char* e = std::getenv("SMG_TRACE");
@@ -2379,6 +2388,7 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.tune = g_tune;
   a.heavy_stream = g_heavy_stream;
   a.heavy_min = g_heavy_min;
+  a.list_cost = g_list_cost;
   a.shard = L.shard;
   a.num_shards = L.num_shards;
   a.ctr = r.ctr;
@@ -2837,6 +2847,7 @@ int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has
   a.tune = g_tune;
   a.heavy_stream = g_heavy_stream;
   a.heavy_min = g_heavy_min;
+  a.list_cost = g_list_cost;
   a.prog = prog;
   unsigned long long total = 0;
   int status = SMG_OK;
