@@ -27,6 +27,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/symmine_gpu.h"
@@ -2561,17 +2562,49 @@ int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_
   if (offsets[0] != 0) return fail(SMG_EINPUT, "offsets[0] must be 0");
   const uint64_t slots = offsets[n];
   if (slots && !adjacency) return fail(SMG_EINPUT, "null adjacency");
+  // Validate the CSR (the reference's Graph invariants, graph.hpp:20-59) on
+  // all host threads: vertex ranges checked independently, first error wins.
   uint64_t maxd = 0;
-  for (uint64_t v = 0; v < n; ++v) {
-    if (offsets[v + 1] < offsets[v]) return fail(SMG_EINPUT, "offsets must be non-decreasing");
-    const uint64_t d = offsets[v + 1] - offsets[v];
-    if (d > maxd) maxd = d;
-    for (uint64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
-      const uint32_t x = adjacency[i];
-      if (x >= n) return fail(SMG_EINPUT, "adjacency id out of range");
-      if (x == v) return fail(SMG_EINPUT, "self loop in adjacency");
-      if (i > offsets[v] && adjacency[i - 1] >= x)
-        return fail(SMG_EINPUT, "neighbour lists must be strictly ascending");
+  {
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const unsigned nth = n < (1u << 16) ? 1u : hw;
+    std::vector<uint64_t> tmax(nth, 0);
+    std::vector<const char*> terr(nth, nullptr);
+    auto check = [&](unsigned t) {
+      const uint64_t v0 = n * t / nth, v1 = n * (t + 1) / nth;
+      uint64_t m = 0;
+      for (uint64_t v = v0; v < v1; ++v) {
+        if (offsets[v + 1] < offsets[v]) {
+          terr[t] = "offsets must be non-decreasing";
+          return;
+        }
+        const uint64_t d = offsets[v + 1] - offsets[v];
+        if (d > m) m = d;
+        for (uint64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
+          const uint32_t x = adjacency[i];
+          if (x >= n) {
+            terr[t] = "adjacency id out of range";
+            return;
+          }
+          if (x == v) {
+            terr[t] = "self loop in adjacency";
+            return;
+          }
+          if (i > offsets[v] && adjacency[i - 1] >= x) {
+            terr[t] = "neighbour lists must be strictly ascending";
+            return;
+          }
+        }
+      }
+      tmax[t] = m;
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(check, t);
+    check(0);
+    for (auto& th : pool) th.join();
+    for (unsigned t = 0; t < nth; ++t) {
+      if (terr[t]) return fail(SMG_EINPUT, terr[t]);
+      maxd = std::max(maxd, tmax[t]);
     }
   }
   if (maxd >= (1ull << 32)) return fail(SMG_EINPUT, "degree too large");
