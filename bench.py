@@ -97,110 +97,146 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- CPU legs ---
-def cpu_sample(graph, plans, seconds, use_reference, threads, seed=2024):
-    """Time the reference CPU engine (oracle/_ref, compiled from /root/reference)
-    -- or the C restatement when that library is absent -- on uniformly drawn
-    single roots (Executor::count_range(v, v+1), engine.cpp:36-43).  Roots are
-    drawn with degree <= 1000 so a few hub roots cannot dominate the bounded
-    sample.  E of the sampled roots comes from the restatement's meter (not
-    timed).  Returns (E/s, info)."""
+def unit_sample(offsets, adjacency, plan, size, seed):
+    """Uniform edge-slot sample of the plan's level-1 units (v0, v1): slots drawn
+    without replacement from those passing level 1's bound (the
+    better estimator; hubs included at their edge share)."""
     import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
-    from oracle.ref import Port, Reference, reference_available
-
-    port = Port()
-    kind = "reference" if (use_reference and reference_available()) else "port"
-    deg = np.diff(graph.offsets)
+    deg = np.diff(offsets.astype(np.int64))
+    src = np.repeat(np.arange(deg.size, dtype=np.uint32), deg)
+    ok = np.ones(adjacency.size, dtype=bool)
+    if plan.to_smg().parent[1] == 0:
+        ok = adjacency < src
+    pool = np.flatnonzero(ok)
     rng = np.random.default_rng(seed)
-    pool_roots = np.flatnonzero((deg > 0) & (deg <= 1000))
-    roots = rng.choice(pool_roots, size=min(len(pool_roots), 200000), replace=False)
-    if kind == "reference":
-        ref = Reference()
-        rg = ref.graph_from_csr(graph.offsets, graph.adjacency)
-        jobs = [(lbl, p.to_json()) for lbl, p in plans]
+    pick = rng.choice(pool, size=min(size, pool.size), replace=False)
+    return pick.astype(np.uint64), src[pick], adjacency[pick]
 
-        def run(root, pj):
-            return rg.count_range(pj, int(root), int(root) + 1)
-    else:
-        jobs = [(lbl, p.to_smg()) for lbl, p in plans]
 
-        def run(root, sp):
-            return port.count_range(graph.offsets, graph.adjacency, sp, int(root), int(root) + 1)[0]
-
-    # calibrate: run roots until the time budget is spent, all threads busy
-    done = []
-    t0 = time.perf_counter()
-    it = iter(roots)
+def sample_elements(offsets, adjacency, plan, slots, threads):
+    """E of the sampled units from the C restatement's meter (untimed)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import numpy as np
+    from oracle.ref import Port
+    port = Port()
+    sp = plan.to_smg()
+    parts = np.array_split(np.asarray(slots, dtype=np.uint64), max(1, threads * 4))
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        futs = []
-        while True:
-            if time.perf_counter() - t0 > seconds:
-                break
-            batch = [next(it, None) for _ in range(threads * 4)]
-            batch = [b for b in batch if b is not None]
-            if not batch:
-                break
-            futs = [(b, ex.submit(lambda b=b: [run(b, j[1]) for j in jobs])) for b in batch]
-            for b, f in futs:
-                done.append((int(b), f.result()))
-    elapsed = time.perf_counter() - t0
-    sample_roots = [b for b, _ in done]
-    # E of the sample (C restatement meter, untimed)
-    E = 0
-    sps = [p.to_smg() for _, p in plans]
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        for part in ex.map(lambda r: sum(port.count_range(graph.offsets, graph.adjacency, sp, r, r + 1)[1]
-                                         for sp in sps), sample_roots):
-            E += part
-    return E / elapsed, {"kind": kind, "cores": threads, "roots": sample_roots, "elapsed_s": elapsed,
-                         "E": E, "counts": [c for _, c in done]}
+        return sum(ex.map(lambda s: port.count_edges(offsets, adjacency, sp, s)[1] if s.size else 0, parts))
+
+
+class CpuReference:
+    """The reference's own CPU engine (oracle/_ref, compiled from
+    /root/reference): Executor::count_from(2) per level-1 unit (the exact path
+    count_range runs for it, engine.cpp:36-43, 89-115), one Executor per host
+    thread, one continuous dynamic queue over the sample.  Falls back to the C
+    restatement's threaded per-unit counts when the reference library is
+    absent (kind "port")."""
+
+    def __init__(self, offsets, adjacency, plans, threads):
+        from oracle.ref import Port, Reference, reference_available
+        self.off, self.adj, self.plans, self.threads = offsets, adjacency, plans, threads
+        self.kind = "reference" if reference_available() else "port"
+        if self.kind == "reference":
+            self.rg = Reference().graph_from_csr(offsets, adjacency)
+        else:
+            self.port = Port()
+
+    def run(self, plan, slots, v0, v1, budget_s=0.0):
+        """Count the units (a prefix of them when budget_s > 0); returns
+        (number counted, their total count, wall seconds)."""
+        import numpy as np
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            c, _ = self.rg.count_units(plan.to_json(), v0, v1, self.threads, budget_s)
+            k, total = len(c), int(c.sum(dtype=np.uint64))
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            sp = plan.to_smg()
+            parts = np.array_split(slots, max(1, self.threads * 8))
+            with ThreadPoolExecutor(max_workers=self.threads) as ex:
+                res = list(ex.map(lambda s: self.port.count_edges(self.off, self.adj, sp, s)[0] if s.size else 0,
+                                  parts))
+            k, total = len(slots), sum(res)
+        return k, total, time.perf_counter() - t0
+
+
+def cpu_sample(graph, plans, seconds, threads, seed=2024):
+    """Calibrate a bounded CPU sample of the workload: per plan, uniformly drawn
+    level-1 units counted by the reference engine on all host threads until
+    seconds/len(plans) elapse.  Returns (E/s, info) with the fixed sample."""
+    cpu = CpuReference(graph.offsets, graph.adjacency, plans, threads)
+    per = seconds / max(1, len(plans))
+    sample, E, elapsed = [], 0, 0.0
+    for i, (label, plan) in enumerate(plans):
+        slots, v0, v1 = unit_sample(graph.offsets, graph.adjacency, plan, 1 << 21, seed + i)
+        k, _, dt = cpu.run(plan, slots, v0, v1, budget_s=per)
+        e = sample_elements(graph.offsets, graph.adjacency, plan, slots[:k], threads)
+        sample.append((label, plan, slots[:k], v0[:k], v1[:k], e))
+        E += e
+        elapsed += dt
+    return E / elapsed, {"kind": cpu.kind, "cores": threads, "elapsed_s": elapsed, "E": E, "cpu": cpu,
+                         "sample": sample, "units": sum(len(x[2]) for x in sample)}
+
+
+def load_graph_file(cfg):
+    """The config's CSR for the reference arm, read from the .npz cache with
+    numpy only.  A cache miss is filled by a separate process (the seeded
+    generator of paper_1911_12877_b200.configs), so no library of this repo is
+    mapped into the reference arm's process."""
+    import numpy as np
+    from types import SimpleNamespace
+    code = ("import sys; sys.path.insert(0, %r); from paper_1911_12877_b200 import configs; "
+            "print(configs.cache_path(%r, fill=True))" % (ROOT, cfg))
+    path = subprocess.run([sys.executable, "-c", code], check=True, capture_output=True,
+                          text=True).stdout.strip().splitlines()[-1]
+    z = np.load(path)
+    off, adj = z["offsets"], z["adjacency"]
+    return SimpleNamespace(offsets=off, adjacency=adj, n=off.size - 1, m=adj.size // 2)
+
+
+def plan_list(cfg):
+    from paper_1911_12877_b200 import configs  # plans + descriptions only: maps no native library
+    return configs.config_patterns(cfg)
+
+
+def describe(cfg):
+    from paper_1911_12877_b200 import configs
+    return configs.describe(cfg)
 
 
 def reference_arm(args):
     """--impl reference: the reference's own CPU engine on this box's host cores."""
-    import numpy as np  # noqa: F401
-    from paper_1911_12877_b200 import configs
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
-    graph = configs.load(CONFIG)
-    plans = configs.config_patterns(CONFIG)
+    graph = load_graph_file(CONFIG)
+    plans = plan_list(CONFIG)
     threads = os.cpu_count() or 1
     # fix the sample once (calibration ~ one step's budget), then time K steps on it
-    step_budget = float(os.environ.get("SMG_REF_STEP_S", "8"))
-    _, info = cpu_sample(graph, plans, step_budget, True, threads)
-    roots = info["roots"]
-    kind = info["kind"]
-    from concurrent.futures import ThreadPoolExecutor
-    from oracle.ref import Port, Reference
-    if kind == "reference":
-        rg = Reference().graph_from_csr(graph.offsets, graph.adjacency)
-        jobs = [p.to_json() for _, p in plans]
-        run = lambda r: [rg.count_range(j, r, r + 1) for j in jobs]  # noqa: E731
-    else:
-        port = Port()
-        jobs = [p.to_smg() for _, p in plans]
-        run = lambda r: [port.count_range(graph.offsets, graph.adjacency, j, r, r + 1)[0] for j in jobs]  # noqa: E731
+    step_budget = float(os.environ.get("SMG_REF_STEP_S", "10"))
+    _, info = cpu_sample(graph, plans, step_budget, threads)
+    cpu = info["cpu"]
     times = []
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        for s in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            list(ex.map(run, roots))
-            dt = time.perf_counter() - t0
-            if s >= args.warmup:
-                times.append(dt)
+    for s in range(args.warmup + args.steps):
+        dt = 0.0
+        for label, plan, slots, v0, v1, _ in info["sample"]:
+            dt += cpu.run(plan, slots, v0, v1)[2]
+        if s >= args.warmup:
+            times.append(dt)
     t = sum(times)
     value = info["E"] * len(times) / t
-    sample = (f"{len(roots)} uniformly drawn roots (degree <= 1000) of {CONFIG}, patterns "
-              f"{[lbl for lbl, _ in plans]}, Executor::count_range per root, {threads} threads")
+    sample = (f"{info['units']} level-1 units drawn uniformly over the edge slots of {CONFIG} "
+              f"({', '.join(f'{lbl}: {len(sl)}' for lbl, _, sl, _, _, _ in info['sample'])}), each counted "
+              f"by the reference's Executor::count_from(2) on a dynamic queue over {threads} threads")
     line = {
         "impl": "reference", "metric": "intersected_elements_per_s", "value": value,
         "unit": "elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded RMAT-20)",
-        "config": {"workload": f"{CONFIG}: {configs.describe(CONFIG)} (root sample)",
-                   "patterns": [lbl for lbl, _ in plans], "sample_roots": len(roots)},
-        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads, "kind": kind,
+        "vs_baseline": None, "dtype": "u32", "data": f"synthetic ({CONFIG}, seeded)",
+        "config": {"workload": f"{CONFIG}: {describe(CONFIG)} (unit sample)",
+                   "patterns": [lbl for lbl, _ in plans], "sample_units": info["units"]},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads, "kind": info["kind"],
                          "sample": sample},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -218,14 +254,16 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def load_profile(cfg, label):
+    """ncu figures (DRAM bytes per count, L2 hit rate) of the dominant count,
+    from the committed summary of this workload (profiles/ncu_summary.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch")
     except Exception:
         return None
+    ent = d.get("workloads", {}).get(f"{cfg}:{label}")
+    return ent
 
 
 def kernels_per_count(plan) -> int:
@@ -358,22 +396,31 @@ def our_arm(args):
     t_e2e = allmax(t_e2e) / e2e_steps
     e2e_value = E_total / t_e2e
 
-    # ---- roofline of the dominant kernel (rank 0's shard) -------------------
+    # ---- roofline of the dominant count (rank 0's shard) ---------------------
+    # Physical: DRAM bytes per count of the dominant pattern (count_kernel +
+    # heavy_kernel, one ncu --set full capture of this workload, committed in
+    # profiles/) / this run's live kernel time for that count / measured HBM
+    # peak.  Algorithmic: 4 B x E (a merge engine's element reads)
+    # / the same time -- reported separately, it is not a roofline.
     dom = max(kern_ms, key=lambda k: statistics.mean(kern_ms[k]))
     dom_ms = statistics.mean(kern_ms[dom])
-    E_dom_local = None
     r = shard(dict(plans)[dom], meter=True)
     E_dom_local = r.elements
-    achieved = 4.0 * E_dom_local / (dom_ms / 1e3) / 1e9
+    alg_gbs = 4.0 * E_dom_local / (dom_ms / 1e3) / 1e9
     peak, peak_kind = load_peaks()
+    prof = load_profile(CONFIG, dom)
+    traffic = prof.get("dram_bytes_per_launch") if prof else None
+    achieved = traffic / (dom_ms / 1e3) / 1e9 if traffic else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu_v, info = cpu_sample(graph, plans, CPU_SAMPLE_SECONDS, True, os.cpu_count() or 1)
+        cpu_v, info = cpu_sample(graph, plans, CPU_SAMPLE_SECONDS, os.cpu_count() or 1)
         cpu = {"value": cpu_v, "unit": "elements/s", "cores": info["cores"], "kind": info["kind"],
-               "sample": (f"{len(info['roots'])} uniformly drawn roots (degree <= 1000) of {CONFIG}, "
-                          f"{[lbl for lbl, _ in plans]} via Executor::count_range, {info['elapsed_s']:.1f} s "
-                          f"on {info['cores']} threads; E of the sample from the oracle meter")}
+               "sample": (f"{info['units']} level-1 units drawn uniformly over the edge slots of {CONFIG} "
+                          f"({', '.join(f'{lbl}: {len(sl)}' for lbl, _, sl, _, _, _ in info['sample'])}), "
+                          f"counted by the reference's Executor::count_from(2) on one dynamic queue over "
+                          f"{info['cores']} threads in {info['elapsed_s']:.1f} s; E of the sample from the "
+                          f"oracle meter (untimed)")}
     if rank == 0:
         line = {
             "metric": "intersected_elements_per_s", "value": value, "unit": "elements/s",
@@ -389,10 +436,15 @@ def our_arm(args):
             "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": load_traffic(),
-                         "kernel": f"count_kernel + heavy_kernel ({dom})", "peak_source": peak_kind,
-                         "note": "achieved = 4 B x E (algorithmic, merge-based) / kernel time; "
-                                 "hoisting and probe-side selection read far fewer bytes"},
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": f"count_kernel + heavy_kernel, one count of {dom}",
+                         "l2_hit_pct": prof.get("l2_hit_pct") if prof else None,
+                         "peak_source": peak_kind,
+                         "traffic_source": prof.get("source") if prof else None,
+                         "algorithmic": {"value": alg_gbs, "unit": "GB/s", "frac_of_peak": alg_gbs / peak,
+                                         "note": "4 B x E / kernel time (E = elements a merge-based level "
+                                                 "build consumes); hoisting, probe-side choice and leaf "
+                                                 "batching read far fewer bytes, so this exceeds HBM"}},
             "gpu_launches": args.steps * sum(kernels_per_count(p) for _, p in plans),
             "clocks": clocks.summary(),
         }

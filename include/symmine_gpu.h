@@ -150,6 +150,20 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
 int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint32_t shard,
                     uint32_t num_shards, uint32_t flags, smg_result* out);
 
+/*
+ * The shard map smg_count / smg_count_shard use for num_shards > 1 (replaces
+ * the reference's static root blocks, engine.cpp:157-158): the level-1 unit
+ * slots are cut into chunks of 32; chunk k costs sum over its slots (v0, v1)
+ * of 1 + min(deg v0, deg v1) (only slots with v1 < v0 when unit_bound); the
+ * chunks are split into J = num_shards * 64 super-chunks of equal cost
+ * (bounds[j] = first chunk k whose exclusive cost prefix P[k] satisfies
+ * P[k] * J >= j * total; bounds[J] = #chunks), and super-chunk j belongs to
+ * shard j % num_shards, which runs a dynamic queue over its super-chunks.
+ * Writes the J + 1 bounds (host array).
+ */
+int smg_shard_bounds(const smg_graph* g, int replica, uint32_t num_shards, int unit_bound,
+                     uint64_t* bounds);
+
 /* Roots [lo, hi) only, like Executor::count_range (engine.cpp:36-43). */
 int smg_count_range(const smg_graph* g, const smg_plan* plan, int replica, uint32_t lo,
                     uint32_t hi, uint32_t flags, smg_result* out);

@@ -12,13 +12,19 @@
 //    (graph.hpp:34-41): adjacency = neighbors(0).data() .. + 2*edge_count(),
 //    offsets rebuilt as neighbors(v).data() - base (size_t -> uint64_t).
 //  * The device replica is cached per Graph object (a Graph is immutable after
-//    construction, graph.hpp:18-19); call release(g) to drop it.
+//    construction, graph.hpp:18-19); call release(g) to drop it.  A cached
+//    entry is reused only if the Graph at that address still has the same
+//    shape, adjacency base pointer and a sampled checksum of its offsets and
+//    adjacency, so a new Graph that lands at a destroyed one's address is
+//    re-uploaded instead of silently counted on stale device data.
 //  * C-ABI status codes are rethrown as the reference's exceptions:
 //    SMG_EINPUT -> InputError, SMG_EOVERFLOW -> CountOverflowError,
 //    SMG_EIO -> IoError (error.hpp:10-22), exactly the CLI's exit-code classes
 //    (tools/main.cpp:20-23).
 #pragma once
 
+#include <algorithm>
+#include <cstdint>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -58,11 +64,50 @@ inline smg_plan lower(const Plan& plan) {
   return p;
 }
 
+// Identity of a Graph's contents, cheap to recompute per call: shape, the
+// adjacency base pointer and a checksum over <= 2 x 65,536 evenly spaced
+// offsets and adjacency entries.
+struct Fingerprint {
+  size_t n = 0, m = 0;
+  const VertexId* base = nullptr;
+  uint64_t sum = 0;
+  bool operator==(const Fingerprint& o) const {
+    return n == o.n && m == o.m && base == o.base && sum == o.sum;
+  }
+};
+
+inline Fingerprint fingerprint(const Graph& g) {
+  Fingerprint f;
+  f.n = g.vertex_count();
+  f.m = g.edge_count();
+  f.base = f.n ? g.neighbors(0).data() : nullptr;
+  uint64_t h = 0x9E3779B97F4A7C15ull ^ (f.n * 31 + f.m);
+  auto mix = [&h](uint64_t x) {
+    h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h *= 0xff51afd7ed558ccdull;
+  };
+  constexpr size_t kSamples = 65536;
+  if (f.n) {
+    const size_t step = std::max<size_t>(1, f.n / kSamples);
+    for (size_t v = 0; v < f.n; v += step) mix(g.degree(static_cast<VertexId>(v)) * 0x100000001ull + v);
+    const size_t slots = 2 * f.m;
+    const size_t astep = std::max<size_t>(1, slots / kSamples);
+    for (size_t i = 0; i < slots; i += astep) mix(f.base[i] ^ (static_cast<uint64_t>(i) << 32));
+  }
+  f.sum = h;
+  return f;
+}
+
+struct Entry {
+  Fingerprint fp;
+  smg_graph* handle = nullptr;
+};
+
 struct Cache {
   std::mutex mu;
-  std::map<std::pair<const Graph*, unsigned>, smg_graph*> replicas;
+  std::map<std::pair<const Graph*, unsigned>, Entry> replicas;
   ~Cache() {
-    for (auto& kv : replicas) smg_graph_destroy(kv.second);
+    for (auto& kv : replicas) smg_graph_destroy(kv.second.handle);
   }
 };
 
@@ -74,8 +119,13 @@ inline Cache& cache() {
 inline smg_graph* replica(const Graph& g, unsigned gpus) {
   Cache& c = cache();
   std::lock_guard<std::mutex> lock(c.mu);
+  const Fingerprint fp = fingerprint(g);
   auto it = c.replicas.find({&g, gpus});
-  if (it != c.replicas.end()) return it->second;
+  if (it != c.replicas.end()) {
+    if (it->second.fp == fp) return it->second.handle;
+    smg_graph_destroy(it->second.handle);  // a different Graph now lives at this address
+    c.replicas.erase(it);
+  }
   const size_t n = g.vertex_count();
   std::vector<uint64_t> offsets(n + 1, 0);
   const VertexId* base = n ? g.neighbors(0).data() : nullptr;
@@ -86,7 +136,7 @@ inline smg_graph* replica(const Graph& g, unsigned gpus) {
   }
   smg_graph* h = nullptr;
   check(smg_graph_create(offsets.data(), base, n, nullptr, static_cast<int>(gpus), &h));
-  c.replicas[{&g, gpus}] = h;
+  c.replicas[{&g, gpus}] = Entry{fp, h};
   return h;
 }
 
@@ -98,7 +148,7 @@ inline void release(const Graph& g) {
   std::lock_guard<std::mutex> lock(c.mu);
   for (auto it = c.replicas.begin(); it != c.replicas.end();) {
     if (it->first.first == &g) {
-      smg_graph_destroy(it->second);
+      smg_graph_destroy(it->second.handle);
       it = c.replicas.erase(it);
     } else {
       ++it;

@@ -76,6 +76,12 @@ class Reference:
             _bind(lib, "ref_count", ctypes.c_int, [_P, _P, ctypes.c_uint, _U64P, ctypes.POINTER(ctypes.c_double)])
             _bind(lib, "ref_count_range", ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, _U64P])
             _bind(lib, "ref_enumerate", ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_uint64, _U32P, ctypes.c_uint64, _U64P])
+            _bind(lib, "ref_count_chunks", ctypes.c_int,
+                  [_P, _P, ctypes.c_uint, _U32P, ctypes.c_uint64, _U64P, _U64P, ctypes.POINTER(ctypes.c_uint8)])
+            _bind(lib, "ref_count_roots", ctypes.c_int,
+                  [_P, _P, ctypes.c_uint, _U32P, ctypes.c_uint64, _U64P, _U64P])
+            _bind(lib, "ref_count_units", ctypes.c_int,
+                  [_P, _P, ctypes.c_uint, _U32P, _U32P, ctypes.c_uint64, _U64P, _U64P, ctypes.c_double, _U64P])
             _bind(lib, "ref_oracle_induced", ctypes.c_int,
                   [_P, ctypes.c_char_p, ctypes.c_int, ctypes.c_char_p, _U64P])
             Reference._lib = lib
@@ -176,6 +182,54 @@ class RefGraph:
             if rc:
                 self.ref._err(rc)
             return c.value
+        finally:
+            self.ref.lib.ref_plan_free(p)
+
+    def count_chunks(self, plan_json, starts, order, counts, done, workers):
+        """Dynamic root-chunk queue (one Executor per thread); fills counts/done
+        in place so a caller thread can checkpoint while it runs."""
+        p = self._plan(plan_json)
+        try:
+            starts = np.ascontiguousarray(starts, dtype=np.uint32)
+            order = np.ascontiguousarray(order, dtype=np.uint64)
+            rc = self.ref.lib.ref_count_chunks(self.h, p, workers, _u32(starts), len(starts) - 1, _u64(order),
+                                               _u64(counts), done.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+            if rc:
+                self.ref._err(rc)
+        finally:
+            self.ref.lib.ref_plan_free(p)
+
+    def count_roots(self, plan_json, roots, workers):
+        """Per-root counts and per-root CPU ns (dynamic queue, one Executor per thread)."""
+        p = self._plan(plan_json)
+        try:
+            roots = np.ascontiguousarray(roots, dtype=np.uint32)
+            counts = np.zeros(max(len(roots), 1), dtype=np.uint64)
+            ns = np.zeros(max(len(roots), 1), dtype=np.uint64)
+            rc = self.ref.lib.ref_count_roots(self.h, p, workers, _u32(roots), len(roots), _u64(counts), _u64(ns))
+            if rc:
+                self.ref._err(rc)
+            return counts[: len(roots)], ns[: len(roots)]
+        finally:
+            self.ref.lib.ref_plan_free(p)
+
+    def count_units(self, plan_json, v0, v1, workers, budget_s=0.0):
+        """Per-unit counts of level-1 units (v0, v1) (the reference's count_from(2))
+        and per-unit CPU ns; dynamic queue, one Executor per thread.  With a
+        budget, only a prefix of the units is counted: the returned arrays are
+        cut to it."""
+        p = self._plan(plan_json)
+        try:
+            v0 = np.ascontiguousarray(v0, dtype=np.uint32)
+            v1 = np.ascontiguousarray(v1, dtype=np.uint32)
+            counts = np.zeros(max(len(v0), 1), dtype=np.uint64)
+            ns = np.zeros(max(len(v0), 1), dtype=np.uint64)
+            done = ctypes.c_uint64()
+            rc = self.ref.lib.ref_count_units(self.h, p, workers, _u32(v0), _u32(v1), len(v0), _u64(counts),
+                                              _u64(ns), float(budget_s), ctypes.byref(done))
+            if rc:
+                self.ref._err(rc)
+            return counts[: done.value], ns[: done.value]
         finally:
             self.ref.lib.ref_plan_free(p)
 

@@ -7,9 +7,29 @@
 // this TU includes that source file to reach Executor::count_range
 // (proj/src/engine.cpp:36-43) for root-range parity; the library build leaves
 // engine.cpp out of its own object list so nothing is defined twice.
-#include SYMMINE_ENGINE_CPP
+// Everything engine.cpp includes comes first, so that the access override
+// below applies to engine.cpp's own Executor only: ref_count_units drives the
+// reference's count_from(2) for single level-1 units (v0, v1) -- the same
+// code path count_range runs for them (engine.cpp:36-43, 89-115).
+#include <array>
+#include <chrono>
+#include <optional>
+#include <span>
+#include <thread>
+#include <vector>
 
+#include "symmine/engine.hpp"
+#include "symmine/error.hpp"
+#include "symmine/set_ops.hpp"
+#define private public
+#include SYMMINE_ENGINE_CPP
+#undef private
+
+#include <atomic>
+#include <chrono>
 #include <cstring>
+#include <thread>
+#include <vector>
 #include <sstream>
 #include <string>
 
@@ -197,6 +217,118 @@ int ref_enumerate(void* g, void* plan, int has_limit, uint64_t limit, uint32_t* 
 
 int ref_oracle_induced(void* g, const char* name, int k, const char* pattern_text, uint64_t* count) {
   return guarded([&] { *count = oracle::induced_count(*static_cast<Graph*>(g), pattern_of(name, k, pattern_text)); });
+}
+
+// Dynamic root queue over all host threads with one Executor per thread (the
+// reference's count_instances uses static root blocks, engine.cpp:157-158,
+// whose slowest block sets the wall time).  Chunk c covers roots
+// [starts[c], starts[c+1]); chunks are claimed in `order`, skipping those with
+// done[c] != 0, and each finished chunk stores its count and sets done[c] = 1
+// (the caller may snapshot both arrays while this runs: checkpoint/resume).
+int ref_count_chunks(void* g, void* plan, unsigned workers, const uint32_t* starts, uint64_t nchunks,
+                     const uint64_t* order, uint64_t* counts, volatile uint8_t* done) {
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> status{0};
+  auto work = [&] {
+    int rc = guarded([&] {
+      Executor exec(*static_cast<Graph*>(g), *static_cast<Plan*>(plan));
+      for (;;) {
+        if (status.load()) return;
+        const uint64_t i = next.fetch_add(1);
+        if (i >= nchunks) return;
+        const uint64_t c = order[i];
+        if (done[c]) continue;
+        counts[c] = exec.count_range(starts[c], starts[c + 1]);
+        std::atomic_thread_fence(std::memory_order_release);
+        done[c] = 1;
+      }
+    });
+    if (rc) status.store(rc);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < std::max(1u, workers); ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  return status.load();
+}
+
+// Per-root counts with the per-root CPU time (ns) of each, one Executor per
+// thread, dynamic queue: the CPU baseline's sampler and hub-root goldens.
+int ref_count_roots(void* g, void* plan, unsigned workers, const uint32_t* roots, uint64_t nroots,
+                    uint64_t* counts, uint64_t* ns) {
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> status{0};
+  auto work = [&] {
+    int rc = guarded([&] {
+      Executor exec(*static_cast<Graph*>(g), *static_cast<Plan*>(plan));
+      for (;;) {
+        if (status.load()) return;
+        const uint64_t i = next.fetch_add(1);
+        if (i >= nroots) return;
+        const auto t0 = std::chrono::steady_clock::now();
+        counts[i] = exec.count_range(roots[i], roots[i] + 1);
+        if (ns)
+          ns[i] = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+      }
+    });
+    if (rc) status.store(rc);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < std::max(1u, workers); ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  return status.load();
+}
+
+// Per-unit counts of level-1 units (v0, v1) = directed edge slots, with the
+// per-unit CPU time (ns): the reference's own count_from(2) after fixing
+// values_[0..1] -- exactly what count_range does for that v1 inside root v0's
+// level-1 loop (engine.cpp:106-113), including the level-1 parent check.
+// Dynamic queue, one Executor per thread.  Used for edge-slot sampling (the
+// CPU baseline) and per-unit goldens.
+// budget_s > 0: stop claiming units once that much wall time has passed;
+// *processed = the number of units counted (always a prefix of the list).
+int ref_count_units(void* gp, void* pp, unsigned workers, const uint32_t* v0s, const uint32_t* v1s,
+                    uint64_t nunits, uint64_t* counts, uint64_t* ns, double budget_s, uint64_t* processed) {
+  const Graph& g = *static_cast<Graph*>(gp);
+  const Plan& plan = *static_cast<Plan*>(pp);
+  if (plan.levels.size() < 2) {
+    g_err = "unit counts need a plan of depth >= 2";
+    return 2;
+  }
+  const int par1 = plan.levels[1].restriction_parent;
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> status{0};
+  const auto start = std::chrono::steady_clock::now();
+  auto work = [&] {
+    int rc = guarded([&] {
+      Executor exec(g, plan);
+      for (;;) {
+        if (status.load()) return;
+        if (budget_s > 0 && std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count() > budget_s)
+          return;
+        const uint64_t i = next.fetch_add(1);
+        if (i >= nunits) return;
+        const auto t0 = std::chrono::steady_clock::now();
+        uint64_t c = 0;
+        if (!(par1 == 0 && v1s[i] >= v0s[i])) {
+          exec.values_[0] = v0s[i];
+          exec.values_[1] = v1s[i];
+          c = plan.levels.size() == 2 ? 1 : exec.count_from(2);
+        }
+        counts[i] = c;
+        if (ns)
+          ns[i] = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+      }
+    });
+    if (rc) status.store(rc);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < std::max(1u, workers); ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  if (processed) *processed = std::min<uint64_t>(next.load(), nunits);
+  return status.load();
 }
 
 }  // extern "C"

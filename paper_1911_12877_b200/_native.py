@@ -115,6 +115,8 @@ def gpu_lib():
             _bind(lib, "smg_count_range", ctypes.c_int,
                   [_P, ctypes.POINTER(SmgPlan), ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
                    ctypes.c_uint32, ctypes.POINTER(SmgResult)])
+            _bind(lib, "smg_shard_bounds", ctypes.c_int,
+                  [_P, ctypes.c_int, ctypes.c_uint32, ctypes.c_int, _U64P])
             if lib.smg_abi_version() != 1:
                 raise IoError("libsymmine_gpu.so ABI version mismatch; rebuild")
             _gpu = lib

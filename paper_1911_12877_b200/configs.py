@@ -94,6 +94,16 @@ def generate(spec: GraphSpec) -> Graph:
     return Graph._from_handle(h)
 
 
+def cache_path(cfg_or_spec, fill: bool = False) -> str:
+    """Path of the config's .npz CSR cache; with fill=True it is generated
+    first when missing."""
+    spec = SPECS[cfg_or_spec] if isinstance(cfg_or_spec, str) else cfg_or_spec
+    path = os.path.join(CACHE, spec.tag + ".npz")
+    if fill and not os.path.exists(path):
+        load(spec, cache=True)
+    return path
+
+
 def load(cfg_or_spec, cache: bool = True, verbose: bool = False) -> Graph:
     spec = SPECS[cfg_or_spec] if isinstance(cfg_or_spec, str) else cfg_or_spec
     path = os.path.join(CACHE, spec.tag + ".npz")

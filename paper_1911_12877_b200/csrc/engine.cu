@@ -39,6 +39,9 @@ namespace smg {
 constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr uint32_t kChunk = 32;  // edge slots per queue grab
+// Multi-GPU shard map: the level-1 unit chunks are cut into num_shards *
+// kShardSplit super-chunks of equal estimated cost, dealt round-robin.
+constexpr uint32_t kShardSplit = 64;
 constexpr unsigned kFull = 0xffffffffu;
 // Per-warp shared-memory hash.  The generic kernel (plans of depth >= 5, the
 // clique-local path) keeps 2048 slots (8 KB) at 3 CTAs/SM; the depth-4 batch
@@ -115,6 +118,12 @@ struct KernelArgs {
   uint32_t heavy_min;     // SMG_HEAVY_MIN: big-probe-set batches stream at least this to be deferred
   float list_cost;        // SMG_LIST_COST
   uint32_t shard, num_shards;
+  // Cost-balanced shard map (num_shards > 1): this shard's super-chunks as
+  // chunk ranges [map_begin[k], map_end[k]) and the exclusive prefix of their
+  // lengths map_pref[0..map_k] (the shard's queue position -> global chunk).
+  const unsigned long long* map_begin;
+  const unsigned long long* map_pref;
+  uint32_t map_k;
   Counters* ctr;
   uint32_t* heavy_items;          // CTA-tier queue (kHeavyItemWords per item), may be null
   unsigned long long heavy_cap;
@@ -1324,7 +1333,13 @@ __global__ void __launch_bounds__(kThreads, SHAPE == kShapeBatch4 ? 8 : 3) count
     unsigned long long chunk = 0;
     if (lane == 0) chunk = atomicAdd(&a.ctr->next_chunk, 1ull);
     chunk = __shfl_sync(kFull, chunk, 0);
-    const uint64_t gchunk = chunk * a.num_shards + a.shard;
+    uint64_t gchunk = chunk;
+    if (a.num_shards > 1) {
+      if (chunk >= a.map_pref[a.map_k]) break;
+      uint32_t k = 0;
+      while (a.map_pref[k + 1] <= chunk) ++k;  // map_k <= kShardSplit: a short scan
+      gchunk = a.map_begin[k] + (chunk - a.map_pref[k]);
+    }
     const uint64_t e0 = a.unit_begin + gchunk * kChunk;
     if (e0 >= a.unit_end) break;
     const uint64_t e = e0 + lane;
@@ -2138,6 +2153,90 @@ __global__ void fill_src_kernel(const unsigned long long* __restrict__ off, uint
   }
 }
 
+// CSR validation on the device (the reference's Graph invariants,
+// graph.hpp:18-20, 55-58): pass 1 checks the offsets and reduces the maximum
+// degree; pass 2 (only after pass 1 succeeded, so every slice is in bounds)
+// checks every slot: id < n, no self loop, strictly ascending, and the
+// reverse slot exists (symmetry, by binary search in the neighbour's list).
+// The first error found sets `err` (codes below); the host maps it to
+// SMG_EINPUT.
+enum { kCsrOk = 0, kCsrOffsets = 1, kCsrRange = 2, kCsrLoop = 3, kCsrOrder = 4, kCsrAsym = 5, kCsrDegree = 6 };
+
+__global__ void validate_offsets_kernel(const unsigned long long* __restrict__ off, uint64_t n,
+                                        uint64_t slots, unsigned int* err, unsigned long long* maxd) {
+  unsigned long long m = 0;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long b = off[v], e = off[v + 1];
+    if (e < b || e > slots) {
+      atomicCAS(err, 0u, static_cast<unsigned>(kCsrOffsets));
+      continue;
+    }
+    m = max(m, e - b);
+  }
+  for (int d = 16; d >= 1; d >>= 1) m = max(m, __shfl_xor_sync(kFull, m, d));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(maxd, m);
+}
+
+__global__ void validate_slots_kernel(const unsigned long long* __restrict__ off,
+                                      const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
+                                      uint64_t n, uint64_t slots, unsigned int* err) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < slots;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = src[i], x = adj[i];
+    unsigned code = kCsrOk;
+    if (x >= n) {
+      code = kCsrRange;
+    } else if (x == v) {
+      code = kCsrLoop;
+    } else if (i > off[v] && adj[i - 1] >= x) {
+      code = kCsrOrder;
+    } else {
+      const unsigned long long b = off[x], e = off[x + 1];
+      if (!contains_dev(adj + b, static_cast<uint32_t>(e - b), v)) code = kCsrAsym;
+    }
+    if (code) atomicCAS(err, 0u, code);
+  }
+}
+
+// Shard map: cost proxy of a chunk of kChunk level-1 units =
+// sum over its slots (v0, v1) of 1 + min(deg v0, deg v1) (the smaller list
+// bounds the unit's level-2 set), counting only units that pass level 1's
+// bound when the plan has one.  Exclusive prefix sums over chunks cut the
+// unit range into J super-chunks of equal cost: bound[j] = first chunk k with
+// P[k] * J >= j * total.  paper_1911_12877_b200/distributed.py mirrors this
+// exactly on the host (shard_slots).
+__global__ void chunk_cost_kernel(const unsigned long long* __restrict__ off, const uint32_t* __restrict__ adj,
+                                  const uint32_t* __restrict__ src, uint64_t slots, uint64_t nchunks,
+                                  int unit_bound, unsigned long long* __restrict__ cost) {
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < nchunks;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long c = 0;
+    const uint64_t e1 = (k + 1) * kChunk < slots ? (k + 1) * kChunk : slots;
+    for (uint64_t e = k * kChunk; e < e1; ++e) {
+      const uint32_t v0 = src[e], v1 = adj[e];
+      if (unit_bound && !(v1 < v0)) continue;
+      const unsigned long long d0 = off[v0 + 1] - off[v0], d1 = off[v1 + 1] - off[v1];
+      c += 1 + min(d0, d1);
+    }
+    cost[k] = c;
+  }
+}
+
+__global__ void shard_bounds_kernel(const unsigned long long* __restrict__ pref, uint64_t nchunks, uint32_t J,
+                                    unsigned long long* __restrict__ bound) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > J) return;
+  const unsigned long long total = pref[nchunks];
+  const unsigned long long target = total * j;  // compare P[k] * J >= target
+  uint64_t lo = 0, hi = nchunks;                 // first k in [0, nchunks] with P[k] * J >= target
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (pref[mid] * J >= target) hi = mid; else lo = mid + 1;
+  }
+  bound[j] = j == J ? nchunks : lo;
+}
+
 // ------------------------------------------------------------------ host ---
 
 thread_local std::string g_last_error;
@@ -2197,6 +2296,11 @@ struct Replica {
   cudaStream_t user_stream = nullptr;  // set by smg_graph_set_stream (not owned)
   cudaStream_t active() const { return user_stream ? user_stream : stream; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // cost-balanced shard map, cached per (num_shards, unit_bound)
+  uint32_t map_shards = 0;
+  int map_unit_bound = -1;
+  std::vector<unsigned long long> map_bounds;          // host copy, J + 1 chunk boundaries
+  unsigned long long* map_dev = nullptr;               // this replica's (begin[K], pref[K+1]) per shard
   std::mutex mu;
 };
 
@@ -2306,6 +2410,65 @@ struct Launch {
   uint32_t shard = 0, num_shards = 1;
 };
 
+// The cost-balanced shard map of `num_shards` shards for plans with/without
+// a level-1 bound, built on r's device and cached on the replica (the graph is
+// immutable).  Caller holds r.mu.
+int ensure_shard_map(const smg_graph& g, Replica& r, uint32_t num_shards, int unit_bound) {
+  if (r.map_shards == num_shards && r.map_unit_bound == unit_bound && r.map_dev) return SMG_OK;
+  const uint64_t nch = (g.slots + kChunk - 1) / kChunk;
+  const uint32_t J = num_shards * kShardSplit;
+  cudaStream_t st = r.active();
+  unsigned long long *cost = nullptr, *pref = nullptr, *bnd = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  std::vector<unsigned long long> bounds(J + 1, 0);
+  cudaError_t e = cudaMalloc(&cost, (nch + 1) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&pref, (nch + 1) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&bnd, (J + 1) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cost, pref, nch + 1, st);
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 4));
+  if (e == cudaSuccess) e = cudaMemsetAsync(cost, 0, (nch + 1) * sizeof(unsigned long long), st);
+  if (e == cudaSuccess && nch) {
+    chunk_cost_kernel<<<r.num_sms * 8, 256, 0, st>>>(r.off, r.adj, r.src, g.slots, nch, unit_bound, cost);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cost, pref, nch + 1, st);
+  if (e == cudaSuccess) {
+    shard_bounds_kernel<<<(J + 256) / 256, 256, 0, st>>>(pref, nch, J, bnd);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(bounds.data(), bnd, (J + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(cost);
+  cudaFree(pref);
+  cudaFree(bnd);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return fail(SMG_EIO, std::string("shard map: ") + cudaGetErrorString(e));
+  // per shard s: begin[K] then pref[K+1]; super-chunk j belongs to shard j % S
+  const uint32_t K = kShardSplit, W = 2 * K + 1;
+  std::vector<unsigned long long> h(static_cast<size_t>(num_shards) * W, 0);
+  for (uint32_t sh = 0; sh < num_shards; ++sh) {
+    unsigned long long* b = h.data() + static_cast<size_t>(sh) * W;
+    unsigned long long* pr = b + K;
+    pr[0] = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint32_t j = k * num_shards + sh;
+      b[k] = bounds[j];
+      pr[k + 1] = pr[k] + (bounds[j + 1] - bounds[j]);
+    }
+  }
+  if (r.map_dev) cudaFree(r.map_dev);
+  r.map_dev = nullptr;
+  r.map_shards = 0;
+  SMG_CUDA(cudaMalloc(&r.map_dev, h.size() * sizeof(unsigned long long)));
+  SMG_CUDA(cudaMemcpy(r.map_dev, h.data(), h.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  r.map_bounds = bounds;
+  r.map_shards = num_shards;
+  r.map_unit_bound = unit_bound;
+  return SMG_OK;
+}
+
 // Enqueue one shard on replica r (asynchronous).  Caller holds r.mu.
 template <bool METER, bool TRACE, int SHAPE>
 int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
@@ -2337,17 +2500,30 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
       r.heavy_scratch_bytes = hs;
     }
   }
+  // Per-warp global work areas (radix index / bitmap of a big probe set): only
+  // plans with a batched leaf use them, and only if they fit next to
+  // everything else (else the kernels fall back to bisection probes).
   const uint64_t bm_words = (g.n + 31) / 32;
-  {
+  bool use_bitmaps = false;
+  if (heavy && !(g_tune & 64u)) {
     const size_t bytes = blocks * kWarpsPerBlock * bm_words * sizeof(uint32_t);
-    if (r.warp_bitmaps_bytes < bytes) {
+    if (r.warp_bitmaps_bytes >= bytes) {
+      use_bitmaps = true;
+    } else {
       if (r.warp_bitmaps) cudaFree(r.warp_bitmaps);
       r.warp_bitmaps = nullptr;
       r.warp_bitmaps_bytes = 0;
-      SMG_CUDA(cudaMalloc(&r.warp_bitmaps, bytes));
-      SMG_CUDA(cudaMemset(r.warp_bitmaps, 0, bytes));
-      SMG_CUDA(cudaDeviceSynchronize());
-      r.warp_bitmaps_bytes = bytes;
+      size_t free_b = 0, total_b = 0;
+      SMG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      if (bytes + (2ull << 30) <= free_b && cudaMalloc(&r.warp_bitmaps, bytes) == cudaSuccess) {
+        SMG_CUDA(cudaMemset(r.warp_bitmaps, 0, bytes));
+        SMG_CUDA(cudaDeviceSynchronize());
+        r.warp_bitmaps_bytes = bytes;
+        use_bitmaps = true;
+      } else {
+        cudaGetLastError();
+        r.warp_bitmaps = nullptr;
+      }
     }
   }
   const bool clique = !METER && prog.clique;
@@ -2392,12 +2568,22 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   a.list_cost = g_list_cost;
   a.shard = L.shard;
   a.num_shards = L.num_shards;
+  a.map_begin = nullptr;
+  a.map_pref = nullptr;
+  a.map_k = 0;
+  if (L.num_shards > 1) {
+    int mrc = ensure_shard_map(g, r, L.num_shards, prog.unit_bound);
+    if (mrc) return mrc;
+    a.map_begin = r.map_dev + static_cast<size_t>(L.shard) * (2 * kShardSplit + 1);
+    a.map_pref = a.map_begin + kShardSplit;
+    a.map_k = kShardSplit;
+  }
   a.ctr = r.ctr;
   a.heavy_items = heavy ? r.heavy_items : nullptr;
   a.heavy_cap = heavy ? kHeavyQueueCap : 0;
   a.heavy_scratch = r.heavy_scratch;
   a.local_rows = clique ? r.local_rows : nullptr;
-  a.warp_bitmaps = !(g_tune & 64u) ? r.warp_bitmaps : nullptr;
+  a.warp_bitmaps = use_bitmaps ? r.warp_bitmaps : nullptr;
   a.bitmap_words = bm_words;
   a.heavy_rows = clique ? r.heavy_rows : nullptr;
   a.prog = prog;
@@ -2543,6 +2729,7 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->src) cudaFree(r->src);
     park_work(*r);  // per-warp scratch, queues and bitmaps go to the device's pool
     if (r->ctr) cudaFree(r->ctr);
+    if (r->map_dev) cudaFree(r->map_dev);
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
     if (r->ev0) cudaEventDestroy(r->ev0);
     if (r->ev1) cudaEventDestroy(r->ev1);
@@ -2562,58 +2749,12 @@ int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_
   if (offsets[0] != 0) return fail(SMG_EINPUT, "offsets[0] must be 0");
   const uint64_t slots = offsets[n];
   if (slots && !adjacency) return fail(SMG_EINPUT, "null adjacency");
-  // Validate the CSR (the reference's Graph invariants, graph.hpp:20-59) on
-  // all host threads: vertex ranges checked independently, first error wins.
-  uint64_t maxd = 0;
-  {
-    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    const unsigned nth = n < (1u << 16) ? 1u : hw;
-    std::vector<uint64_t> tmax(nth, 0);
-    std::vector<const char*> terr(nth, nullptr);
-    auto check = [&](unsigned t) {
-      const uint64_t v0 = n * t / nth, v1 = n * (t + 1) / nth;
-      uint64_t m = 0;
-      for (uint64_t v = v0; v < v1; ++v) {
-        if (offsets[v + 1] < offsets[v]) {
-          terr[t] = "offsets must be non-decreasing";
-          return;
-        }
-        const uint64_t d = offsets[v + 1] - offsets[v];
-        if (d > m) m = d;
-        for (uint64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
-          const uint32_t x = adjacency[i];
-          if (x >= n) {
-            terr[t] = "adjacency id out of range";
-            return;
-          }
-          if (x == v) {
-            terr[t] = "self loop in adjacency";
-            return;
-          }
-          if (i > offsets[v] && adjacency[i - 1] >= x) {
-            terr[t] = "neighbour lists must be strictly ascending";
-            return;
-          }
-        }
-      }
-      tmax[t] = m;
-    };
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(check, t);
-    check(0);
-    for (auto& th : pool) th.join();
-    for (unsigned t = 0; t < nth; ++t) {
-      if (terr[t]) return fail(SMG_EINPUT, terr[t]);
-      maxd = std::max(maxd, tmax[t]);
-    }
-  }
-  if (maxd >= (1ull << 32)) return fail(SMG_EINPUT, "degree too large");
   int ndev = smg_device_count();
   if (ndev == 0) return fail(SMG_EIO, "no CUDA device available (the engine has no CPU path)");
   smg_graph* g = new smg_graph;
   g->n = n;
   g->slots = slots;
-  g->max_degree = maxd;
+  g->max_degree = 0;
   for (int i = 0; i < num_devices; ++i) {
     const int dev = devices ? devices[i] : i;
     if (dev < 0 || dev >= ndev) {
@@ -2643,9 +2784,46 @@ int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_
               step(cudaMallocHost(&r->host_ctr, sizeof(Counters)), "cudaMallocHost") &&
               step(cudaMemcpyAsync(r->off, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, r->stream), "H2D offsets") &&
               (slots == 0 || step(cudaMemcpyAsync(r->adj, adjacency, slots * sizeof(uint32_t), cudaMemcpyHostToDevice, r->stream), "H2D adjacency"));
-    if (ok && n > 0) {
+    // Replica 0 is validated on its device (later copies are byte-identical):
+    // offsets first (so every slice is in bounds), then the slot map, then
+    // the slots themselves.
+    unsigned int herr = 0;
+    unsigned long long hmax = 0;
+    unsigned int* derr = reinterpret_cast<unsigned int*>(&r->ctr->overflow);
+    unsigned long long* dmax = &r->ctr->count;
+    if (ok && i == 0) {
+      ok = step(cudaMemsetAsync(r->ctr, 0, sizeof(Counters), r->stream), "memset");
+      if (ok && n > 0) {
+        validate_offsets_kernel<<<r->num_sms * 4, 256, 0, r->stream>>>(r->off, n, slots, derr, dmax);
+        ok = step(cudaGetLastError(), "validate offsets") &&
+             step(cudaMemcpyAsync(&herr, derr, sizeof(herr), cudaMemcpyDeviceToHost, r->stream), "D2H") &&
+             step(cudaStreamSynchronize(r->stream), "validate offsets");
+      }
+    }
+    if (ok && !herr && n > 0) {
       fill_src_kernel<<<r->num_sms * 8, 256, 0, r->stream>>>(r->off, n, r->src);
       ok = step(cudaGetLastError(), "fill_src");
+    }
+    if (ok && i == 0 && !herr && n > 0) {
+      if (slots > 0) {
+        validate_slots_kernel<<<r->num_sms * 8, 256, 0, r->stream>>>(r->off, r->adj, r->src, n, slots, derr);
+        ok = step(cudaGetLastError(), "validate slots");
+      }
+      ok = ok && step(cudaMemcpyAsync(&herr, derr, sizeof(herr), cudaMemcpyDeviceToHost, r->stream), "D2H") &&
+           step(cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, r->stream), "D2H") &&
+           step(cudaStreamSynchronize(r->stream), "validate slots");
+    }
+    if (ok && i == 0) {
+      if (herr || hmax >= (1ull << 32)) {
+        static const char* msgs[] = {"degree too large",
+                                     "offsets must be non-decreasing and end at the slot count",
+                                     "adjacency id out of range", "self loop in adjacency",
+                                     "neighbour lists must be strictly ascending",
+                                     "adjacency must be symmetric (missing reverse edge)"};
+        smg_graph_destroy(g);
+        return fail(SMG_EINPUT, msgs[herr < 6 ? herr : 0]);
+      }
+      g->max_degree = hmax;
     }
     ok = ok && step(cudaStreamSynchronize(r->stream), "upload");
     if (!ok) {
@@ -2657,10 +2835,12 @@ int smg_graph_create(const uint64_t* offsets, const uint32_t* adjacency, uint64_
   return SMG_OK;
 }
 
-// Runtime parts of a replica (stream, events, counters) on `dev`.
-static int init_replica_runtime(Replica* r, int dev) {
+// Runtime parts of a replica (stream, events, counters) on `dev`.  Only a
+// replica that is kept (`keep`) adopts the device's parked work buffers; a
+// temporary one (smg_graph_from_edges' build stream) must not, or they leak.
+static int init_replica_runtime(Replica* r, int dev, bool keep) {
   r->device = dev;
-  adopt_work(*r);
+  if (keep) adopt_work(*r);
   SMG_CUDA(cudaSetDevice(dev));
   SMG_CUDA(cudaDeviceGetAttribute(&r->num_sms, cudaDevAttrMultiProcessorCount, dev));
   SMG_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
@@ -2680,7 +2860,7 @@ static int adopt_device_csr(const DevCSR& csr, const int* devs, int ndevs, smg_g
   for (int i = 0; i < ndevs; ++i) {
     Replica* r = new Replica;
     g->reps.push_back(r);
-    int rc = init_replica_runtime(r, devs[i]);
+    int rc = init_replica_runtime(r, devs[i], true);
     if (rc) {
       if (i == 0) {  // still owns the arrays
         cudaFree(csr.off);
@@ -2728,18 +2908,24 @@ int smg_graph_from_edges(const uint32_t* pairs, uint64_t num_edges, uint64_t n, 
     if (devs[i] < 0 || devs[i] >= ndev) return fail(SMG_EINPUT, "device index out of range");
   }
   Replica tmp;
-  int rc = init_replica_runtime(&tmp, devs[0]);
-  if (rc) return rc;
+  int rc = init_replica_runtime(&tmp, devs[0], false);
+  auto release_tmp = [&tmp] {
+    if (tmp.stream) cudaStreamDestroy(tmp.stream);
+    if (tmp.ev0) cudaEventDestroy(tmp.ev0);
+    if (tmp.ev1) cudaEventDestroy(tmp.ev1);
+    if (tmp.ctr) cudaFree(tmp.ctr);
+    if (tmp.host_ctr) cudaFreeHost(tmp.host_ctr);
+    tmp.stream = nullptr;
+  };
+  if (rc) {
+    release_tmp();
+    return rc;
+  }
   DevCSR csr;
   uint64_t d = 0, l = 0;
   std::string err;
   rc = device_from_edges(devs[0], tmp.stream, tmp.num_sms, pairs, num_edges, n, &csr, &d, &l, &err);
-  cudaStreamDestroy(tmp.stream);
-  cudaEventDestroy(tmp.ev0);
-  cudaEventDestroy(tmp.ev1);
-  cudaFree(tmp.ctr);
-  cudaFreeHost(tmp.host_ctr);
-  tmp.stream = nullptr;
+  release_tmp();
   if (rc) return fail(rc == 2 ? SMG_EINPUT : SMG_EIO, err);
   if (dups) *dups = d;
   if (loops) *loops = l;
@@ -2933,6 +3119,19 @@ int smg_enumerate(const smg_graph* g, const smg_plan* plan, int replica, int has
   return status;
 }
 
+int smg_shard_bounds(const smg_graph* g, int replica, uint32_t num_shards, int unit_bound, uint64_t* bounds) {
+  if (!g || !bounds) return fail(SMG_EINPUT, "null argument");
+  if (replica < 0 || replica >= static_cast<int>(g->reps.size())) return fail(SMG_EINPUT, "bad replica");
+  if (num_shards == 0 || num_shards > 4096) return fail(SMG_EINPUT, "bad shard count");
+  Replica& r = *g->reps[replica];
+  std::lock_guard<std::mutex> lock(r.mu);
+  SMG_CUDA(cudaSetDevice(r.device));
+  int rc = ensure_shard_map(*g, r, num_shards, unit_bound ? 1 : 0);
+  if (rc) return rc;
+  std::memcpy(bounds, r.map_bounds.data(), r.map_bounds.size() * sizeof(uint64_t));
+  return SMG_OK;
+}
+
 int smg_count_range(const smg_graph* g, const smg_plan* plan, int replica, uint32_t lo,
                     uint32_t hi, uint32_t flags, smg_result* out) {
   const double t0 = now_ms();
@@ -2990,7 +3189,19 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
     L.shard = d;
     L.num_shards = num_gpus;
     rc = enqueue(*g, *g->reps[d], prog, L);
-    if (rc) return rc;
+    if (rc) {
+      // devices 0..d-1 are still counting into their Counters: drain them
+      // before the replica locks are released
+      const std::string err = g_last_error;
+      for (unsigned e = 0; e < d; ++e) {
+        uint64_t c = 0, el = 0, u = 0;
+        bool ovf = false;
+        double ms = 0;
+        finish(*g->reps[e], &c, &el, &u, &ovf, &ms);
+      }
+      g_last_error = err;
+      return rc;
+    }
   }
   bool any_ovf = false;
   for (unsigned d = 0; d < num_gpus; ++d) {

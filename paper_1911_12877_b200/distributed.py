@@ -15,16 +15,60 @@ from . import _native as N
 from .engine import CountResult, count_shard
 
 
-SHARD_CHUNK = 32  # kChunk in csrc/engine.cu: edge slots per work-queue grab
+SHARD_CHUNK = 32   # kChunk in csrc/engine.cu: edge slots per work-queue grab
+SHARD_SPLIT = 64   # kShardSplit: super-chunks per shard
 
 
-def shard_slots(num_slots: int, shard: int, num_shards: int):
-    """The edge slots shard `shard` of `num_shards` owns: global chunk g (slots
-    [32g, 32g+32)) belongs to shard g % num_shards -- the mapping count_kernel
-    applies to its dynamic queue (gchunk = chunk * num_shards + shard)."""
+def chunk_costs(offsets, adjacency, unit_bound: bool):
+    """Cost proxy per chunk of SHARD_CHUNK level-1 units (chunk_cost_kernel):
+    sum over its slots (v0, v1) of 1 + min(deg v0, deg v1), only slots with
+    v1 < v0 when the plan bounds level 1."""
     import numpy as np
-    e = np.arange(num_slots, dtype=np.uint64)
-    return e[(e // SHARD_CHUNK) % num_shards == shard]
+    off = np.asarray(offsets, dtype=np.int64)
+    adj = np.asarray(adjacency, dtype=np.int64)
+    deg = np.diff(off)
+    src = np.repeat(np.arange(deg.size, dtype=np.int64), deg)
+    c = 1 + np.minimum(deg[src], deg[adj]) if adj.size else np.zeros(0, dtype=np.int64)
+    if unit_bound and adj.size:
+        c = np.where(adj < src, c, 0)
+    nch = (adj.size + SHARD_CHUNK - 1) // SHARD_CHUNK
+    if nch == 0:
+        return np.zeros(0, dtype=np.int64)
+    return np.add.reduceat(c, np.arange(0, adj.size, SHARD_CHUNK))
+
+
+def shard_bounds(offsets, adjacency, num_shards: int, unit_bound: bool):
+    """The J + 1 = num_shards * SHARD_SPLIT + 1 super-chunk boundaries of equal
+    estimated cost (smg_shard_bounds / shard_bounds_kernel): bound[j] = first
+    chunk k with P[k] * J >= j * total, P the exclusive cost prefix."""
+    import numpy as np
+    cost = chunk_costs(offsets, adjacency, unit_bound)
+    nch = cost.size
+    pref = np.zeros(nch + 1, dtype=np.int64)
+    np.cumsum(cost, out=pref[1:])
+    J = num_shards * SHARD_SPLIT
+    total = int(pref[-1])
+    # smallest k with pref[k] * J >= j * total (pref is non-decreasing)
+    out = np.array([int(np.searchsorted(pref * J, j * total, side="left")) for j in range(J + 1)],
+                   dtype=np.int64)
+    out[J] = nch
+    return out
+
+
+def shard_slots(offsets, adjacency, shard: int, num_shards: int, unit_bound: bool = False):
+    """The edge slots shard `shard` of `num_shards` owns: super-chunk j (chunks
+    [bound[j], bound[j+1]) of 32 slots) belongs to shard j % num_shards -- the
+    map count_kernel walks with its per-shard dynamic queue.  One shard owns
+    every slot."""
+    import numpy as np
+    nslots = int(np.asarray(adjacency).size)
+    e = np.arange(nslots, dtype=np.uint64)
+    if num_shards == 1:
+        return e
+    b = shard_bounds(offsets, adjacency, num_shards, unit_bound)
+    chunk = e // SHARD_CHUNK
+    j = np.searchsorted(b, chunk, side="right") - 1  # super-chunk of each slot
+    return e[(j % num_shards) == shard]
 
 
 def split_u64(values):

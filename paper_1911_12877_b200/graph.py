@@ -212,6 +212,13 @@ def _check_csr(off: np.ndarray, adj: np.ndarray) -> None:
         same = src[1:] == src[:-1]
         if (adj[1:][same] <= adj[:-1][same]).any():
             raise N.InputError("neighbour lists must be strictly ascending")
+        # symmetry (graph.hpp:18-19): every slot (v, x) has its reverse (x, v);
+        # rows ascending + lists ascending -> the keys are already sorted
+        keys = src * n + adj.astype(np.int64)
+        rev = adj.astype(np.int64) * n + src
+        pos = np.minimum(np.searchsorted(keys, rev), keys.size - 1)
+        if (keys[pos] != rev).any():
+            raise N.InputError("adjacency must be symmetric (missing reverse edge)")
 
 
 def _to_handle(g: Graph):

@@ -39,7 +39,7 @@ def _worker(rank, world, port, q):
         g = Graph.from_edges(*er_graph(30, 0.5, 77))
 
         def cpu_shard(graph, plan, shard, num_shards, device=0, meter=False):
-            slots = shard_slots(graph.adjacency.size, shard, num_shards)
+            slots = shard_slots(graph.offsets, graph.adjacency, shard, num_shards, plan.to_smg().parent[1] == 0)
             c, e = pt.count_edges(graph.offsets, graph.adjacency, plan.to_smg(), slots)
             return CountResult(c, [c], e, len(slots))
 
@@ -80,9 +80,22 @@ def test_gloo_world2_shards_sum_to_full_count():
 
 
 def test_shard_slots_partition():
-    from paper_1911_12877_b200.distributed import shard_slots
     import numpy as np
-    for n in (0, 1, 31, 32, 33, 1000):
-        for s in (1, 2, 3, 8):
-            parts = np.concatenate([shard_slots(n, i, s) for i in range(s)])
-            assert sorted(parts.tolist()) == list(range(n))
+    from paper_1911_12877_b200 import Graph
+    from paper_1911_12877_b200.distributed import SHARD_CHUNK, chunk_costs, shard_bounds, shard_slots
+    for n, p, seed in ((1, 0.0, 1), (30, 0.5, 77), (200, 0.05, 5), (400, 0.3, 9)):
+        g = Graph.from_edges(*er_graph(n, p, seed)) if n > 1 else Graph.from_edges(1, [])
+        for ub in (False, True):
+            for s in (1, 2, 3, 8):
+                parts = np.concatenate([shard_slots(g.offsets, g.adjacency, i, s, ub) for i in range(s)])
+                assert sorted(parts.tolist()) == list(range(g.adjacency.size))
+                if s > 1 and g.adjacency.size:
+                    b = shard_bounds(g.offsets, g.adjacency, s, ub)
+                    assert b[0] == 0 and b[-1] == (g.adjacency.size + SHARD_CHUNK - 1) // SHARD_CHUNK
+                    assert (np.diff(b) >= 0).all()
+                    # equal-cost cut: every super-chunk's cost is within one chunk of total / J
+                    c = chunk_costs(g.offsets, g.adjacency, ub)
+                    pref = np.concatenate([[0], np.cumsum(c)])
+                    J = len(b) - 1
+                    per = pref[b[1:]] - pref[b[:-1]]
+                    assert per.max() <= pref[-1] / J + c.max() + 1

@@ -72,20 +72,60 @@ def test_shards_partition_units(golden, corpus_graphs):
 
 
 def test_shard_units_follow_host_mapping(golden, corpus_graphs, port):
-    """The device's chunk->shard map is the one distributed.shard_slots states
-    (the gloo test relies on it)."""
-    from paper_1911_12877_b200.distributed import shard_slots
-    g = corpus_graphs["er_30_0.6_3030"]
-    src = np.repeat(np.arange(g.n), np.diff(g.offsets).astype(np.int64))
-    p = Plan.from_json(golden["plans"]["house"])
-    for s in (2, 3):
-        for i in range(s):
-            slots = shard_slots(g.adjacency.size, i, s).astype(np.int64)
-            valid = int((g.adjacency[slots] < src[slots]).sum())
-            r = count_shard(g, p, i, s)
-            assert r.units == valid
-            c, _ = port.count_edges(g.offsets, g.adjacency, p.to_smg(), slots)
-            assert r.count == c
+    """The device's cost-balanced chunk->shard map is the one
+    distributed.shard_slots states (the gloo test relies on it): same super-chunk
+    bounds (smg_shard_bounds), same units and counts per shard."""
+    import ctypes
+    from paper_1911_12877_b200 import _native as N
+    from paper_1911_12877_b200.distributed import shard_bounds, shard_slots
+    for gname in ("er_30_0.6_3030", "er_30_0.3_4030"):
+        g = corpus_graphs[gname]
+        src = np.repeat(np.arange(g.n), np.diff(g.offsets).astype(np.int64))
+        h = g.device_handle((0,))
+        for s in (2, 3, 8):
+            for ub in (0, 1):
+                J = s * 64
+                dev = np.zeros(J + 1, dtype=np.uint64)
+                N.check_gpu(N.gpu_lib().smg_shard_bounds(h, 0, s, ub,
+                                                         dev.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+                assert dev.tolist() == shard_bounds(g.offsets, g.adjacency, s, bool(ub)).tolist()
+        for pname in ("house", "pentagon", "clique:4"):
+            p = Plan.from_json(golden["plans"][pname])
+            ub = p.to_smg().parent[1] == 0
+            for s in (2, 3):
+                for i in range(s):
+                    slots = shard_slots(g.offsets, g.adjacency, i, s, ub).astype(np.int64)
+                    valid = int((g.adjacency[slots] < src[slots]).sum()) if ub else slots.size
+                    r = count_shard(g, p, i, s)
+                    assert r.units == valid
+                    c, _ = port.count_edges(g.offsets, g.adjacency, p.to_smg(), slots)
+                    assert r.count == c
+
+
+def test_device_csr_validation_rejects_bad_layouts():
+    """smg_graph_create validates on the device (graph.hpp:18-20, 55-58):
+    asymmetric, unsorted, self-looped or out-of-range adjacency -> InputError."""
+    import ctypes
+    from paper_1911_12877_b200 import _native as N
+    lib = N.gpu_lib()
+
+    def create(off, adj):
+        off = np.asarray(off, dtype=np.uint64)
+        adj = np.asarray(adj if len(adj) else [0], dtype=np.uint32)
+        h = ctypes.c_void_p()
+        rc = lib.smg_graph_create(off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                  adj.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), off.size - 1,
+                                  None, 1, ctypes.byref(h))
+        if rc == 0:
+            lib.smg_graph_destroy(h)
+        return rc, lib.smg_last_error().decode()
+
+    assert create([0, 1, 2], [1, 0])[0] == 0                       # edge 0-1
+    assert create([0, 1, 1], [1]) == (N.SMG_EINPUT, "adjacency must be symmetric (missing reverse edge)")
+    assert create([0, 1, 2], [0, 0])[0] == N.SMG_EINPUT             # self loop
+    assert create([0, 2, 3, 4], [2, 1, 0, 0])[0] == N.SMG_EINPUT    # unsorted list
+    assert create([0, 1, 2], [5, 0])[0] == N.SMG_EINPUT             # id out of range
+    assert create([0, 2, 1], [1, 0])[0] == N.SMG_EINPUT             # decreasing offsets
 
 
 def test_invalid_plan_raises_input_error():
