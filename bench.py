@@ -266,14 +266,25 @@ def load_profile(cfg, label):
     return ent
 
 
-def kernels_per_count(plan) -> int:
-    """count_kernel, plus heavy_kernel when the plan's leaf is batched."""
+# kernels one count launches: the generic executor runs count_kernel (+
+# heavy_kernel for batched leaves); the folded kinds (tindex.cu) run one kernel
+# (star4, tailed diamond a, tailed triangle, diamond), or a center-table pass,
+# an ego-network pass and a combine (house, tailed diamond b), or a center pass
+# and a combine (path4).  The triangle index is built once per graph (cached).
+FOLDED_LAUNCHES = {1: 1, 2: 1, 3: 3, 4: 3, 5: 1, 6: 1, 7: 2}
+
+
+def kernels_per_count(plan):
+    """(kernel launches per count, folded kind or 0)."""
     import ctypes
     from paper_1911_12877_b200 import _native as N
     sp = plan.to_smg()
     buf = ctypes.create_string_buffer(1 << 16)
     N.check_gpu(N.gpu_lib().smg_plan_describe(ctypes.byref(sp), buf, 1 << 16))
-    return 2 if json.loads(buf.value.decode())["batch"] else 1
+    d = json.loads(buf.value.decode())
+    if d.get("fast"):
+        return FOLDED_LAUNCHES[d["fast"]], d["fast"]
+    return (2 if d["batch"] else 1), 0
 
 
 def our_arm(args):
@@ -326,13 +337,17 @@ def our_arm(args):
                                         N.SMG_METER if meter else 0, ctypes.byref(r)))
         return r
 
-    # metering pass: E per pattern (deterministic property of graph + plan)
+    # metering pass: E per pattern (deterministic property of graph + plan).
+    # Plans that lower to a folded closed-form kernel (csrc/tindex.cu) never
+    # enumerate the merges E counts; a config with one reports count time.
+    folded = {label: kernels_per_count(plan)[1] for label, plan in plans}
+    metered = not any(folded.values())
     E, counts = {}, {}
     for label, plan in plans:
-        r = shard(plan, meter=True)
+        r = shard(plan, meter=metered)
         c, e = allsum_u64([r.count, r.elements])
-        E[label], counts[label] = e, c
-    E_total = sum(E.values())
+        E[label], counts[label] = (e if metered else None), c
+    E_total = sum(E.values()) if metered else None
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -366,7 +381,7 @@ def our_arm(args):
     for cs in step_counts:
         tot = allsum_u64(cs)
         assert tot == [counts[lbl] for lbl, _ in plans], (tot, counts)
-    value = E_total / t_step
+    value = E_total / t_step if metered else t_step
 
     # ---- e2e: public C-ABI path from pinned host buffers, every step ------
     off_pin = torch.from_numpy(graph.offsets.view(np.int64)).pin_memory()
@@ -394,7 +409,7 @@ def our_arm(args):
         if s > 0:  # first iteration warms the allocator / context
             t_e2e += dt
     t_e2e = allmax(t_e2e) / e2e_steps
-    e2e_value = E_total / t_e2e
+    e2e_value = E_total / t_e2e if metered else t_e2e
 
     # ---- roofline of the dominant count (rank 0's shard) ---------------------
     # Physical: DRAM bytes per count of the dominant pattern (count_kernel +
@@ -404,9 +419,10 @@ def our_arm(args):
     # / the same time -- reported separately, it is not a roofline.
     dom = max(kern_ms, key=lambda k: statistics.mean(kern_ms[k]))
     dom_ms = statistics.mean(kern_ms[dom])
-    r = shard(dict(plans)[dom], meter=True)
-    E_dom_local = r.elements
-    alg_gbs = 4.0 * E_dom_local / (dom_ms / 1e3) / 1e9
+    alg_gbs = None
+    if not folded[dom]:
+        r = shard(dict(plans)[dom], meter=True)
+        alg_gbs = 4.0 * r.elements / (dom_ms / 1e3) / 1e9
     peak, peak_kind = load_peaks()
     prof = load_profile(CONFIG, dom)
     traffic = prof.get("dram_bytes_per_launch") if prof else None
@@ -422,30 +438,37 @@ def our_arm(args):
                           f"{info['cores']} threads in {info['elapsed_s']:.1f} s; E of the sample from the "
                           f"oracle meter (untimed)")}
     if rank == 0:
+        metric, unit = (("intersected_elements_per_s", "elements/s") if metered else
+                        ("pattern_count_time_s", "s"))
+        if cpu and not metered:
+            cpu["note"] = "elements/s of the reference on a unit sample; this config's E is not metered"
         line = {
-            "metric": "intersected_elements_per_s", "value": value, "unit": "elements/s",
+            "metric": metric, "value": value, "unit": unit,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": t_step * 1e3, "higher_is_better": metered, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32",
             "data": f"synthetic ({configs.describe(CONFIG)}; seeded, no public dataset named)",
             "config": {"workload": f"{CONFIG}: {configs.describe(CONFIG)} (n={graph.n}, m={graph.m})",
                        "patterns": [lbl for lbl, _ in plans], "counts": counts,
                        "elements": E, "pattern_ms": {k: statistics.mean(v) for k, v in kern_ms.items()},
+                       "folded_kernels": {k: v for k, v in folded.items() if v},
                        "parallelism": f"units sharded over {world} GPU(s), 1 allreduce",
                        "l2": "flushed between timed steps (512 MB write)"},
-            "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": f"count_kernel + heavy_kernel, one count of {dom}",
+                         "kernel": (f"folded kind {folded[dom]} (tindex.cu), one count of {dom}" if folded[dom]
+                                    else f"count_kernel + heavy_kernel, one count of {dom}"),
                          "l2_hit_pct": prof.get("l2_hit_pct") if prof else None,
                          "peak_source": peak_kind,
                          "traffic_source": prof.get("source") if prof else None,
-                         "algorithmic": {"value": alg_gbs, "unit": "GB/s", "frac_of_peak": alg_gbs / peak,
+                         "algorithmic": {"value": alg_gbs, "unit": "GB/s",
+                                         "frac_of_peak": (alg_gbs / peak) if alg_gbs else None,
                                          "note": "4 B x E / kernel time (E = elements a merge-based level "
                                                  "build consumes); hoisting, probe-side choice and leaf "
                                                  "batching read far fewer bytes, so this exceeds HBM"}},
-            "gpu_launches": args.steps * sum(kernels_per_count(p) for _, p in plans),
+            "gpu_launches": args.steps * sum(kernels_per_count(p)[0] for _, p in plans),
             "clocks": clocks.summary(),
         }
         if cpu:

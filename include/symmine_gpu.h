@@ -48,6 +48,10 @@ extern "C" {
 
 /* flags argument of the count calls */
 #define SMG_METER 1u /* also compute E, the intersected-element count */
+/* Run the generic plan executor even where a folded closed-form kernel exists
+ * for the plan (the folded kernels, tindex.cu, never meter E: SMG_METER also
+ * selects the generic executor).  For A/B parity checks. */
+#define SMG_GENERIC 2u
 
 /*
  * One compiled plan, the POD image of symmine::Plan (plan.hpp:25-37) as

@@ -23,6 +23,7 @@ MAX_LEVELS = 8
 MAX_GPUS = 8
 
 SMG_OK, SMG_EIO, SMG_EINPUT, SMG_EOVERFLOW = 0, 1, 2, 3
+SMG_GENERIC = 2  # flag: plan executor even where a folded kernel exists
 SMG_PLAN_USE_BOUNDS = 1
 SMG_PLAN_USE_RESTRICTIONS = 2
 SMG_METER = 1

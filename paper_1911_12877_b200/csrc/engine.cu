@@ -33,6 +33,7 @@
 #include "../../include/symmine_gpu.h"
 #include "graph_build.hpp"
 #include "program.hpp"
+#include "tindex.hpp"
 
 namespace smg {
 
@@ -2256,6 +2257,11 @@ const float g_list_cost = [] {
   const char* e = std::getenv("SMG_LIST_COST");
   return e ? static_cast<float>(std::atof(e)) : kListCost;
 }();
+// SMG_FAST=0 disables the folded kernels (tindex.cu) for every call.
+const int g_fast = [] {
+  const char* e = std::getenv("SMG_FAST");
+  return (e && *e == '0') ? 0 : 1;
+}();
 const int g_trace = [] {
   const char* e = std::getenv("SMG_TRACE");
   return (e && *e && *e != '0') ? 1 : 0;
@@ -2301,6 +2307,13 @@ struct Replica {
   int map_unit_bound = -1;
   std::vector<unsigned long long> map_bounds;          // host copy, J + 1 chunk boundaries
   unsigned long long* map_dev = nullptr;               // this replica's (begin[K], pref[K+1]) per shard
+  TIndex tix;                                          // triangle index (folded kernels), built on demand
+  uint32_t* fast_scratch = nullptr;                    // per-warp scratch of the folded kernels
+  size_t fast_scratch_bytes = 0;
+  unsigned long long* fast_acc = nullptr;              // per-slot accumulators (two-center kinds)
+  size_t fast_acc_bytes = 0;
+  uint32_t* fast_dense = nullptr;                      // per-CTA dense codegree tables
+  size_t fast_dense_bytes = 0;
   std::mutex mu;
 };
 
@@ -2606,6 +2619,99 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   return SMG_OK;
 }
 
+// The folded closed-form path (tindex.cu) for plans fast_kind() recognises:
+// builds the triangle index on first use (cached on the replica), then one
+// persistent kernel over the level-1 unit slots.  Same Counters, events and
+// result path as enqueue().  Caller holds r.mu.
+int enqueue_fast(const smg_graph& g, Replica& r, int kind, const smg_plan& plan, const Launch& L) {
+  SMG_CUDA(cudaSetDevice(r.device));
+  cudaStream_t st = r.active();
+  std::string err;
+  const auto tb0 = std::chrono::steady_clock::now();
+  if (tindex_build(&r.tix, r.off, r.adj, r.src, g.n, g.slots, r.num_sms, st, kind == kFastStar4,
+                   kind == kFastTailedDiamondA, &err)) {
+    tindex_free(&r.tix);
+    return fail(SMG_EIO, "triangle index: " + err);
+  }
+  if (g_trace)
+    std::fprintf(stderr, "[smg trace] triangle index ready in %.1f ms (%llu entries, kind %d)\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb0).count(),
+                 static_cast<unsigned long long>(r.tix.entries), kind);
+  const bool dense = fast_dense(kind);
+  const unsigned blocks = static_cast<unsigned>(r.num_sms) * (dense ? 2 : 4);
+  const uint64_t words = fast_scratch_words(kind, g.max_degree);
+  // per-slot accumulators and dense per-CTA codegree tables (two-center kinds)
+  const size_t acc_need = static_cast<size_t>(fast_slot_arrays(kind)) * std::max<uint64_t>(g.slots, 1) * 8;
+  const size_t dense_need = dense ? static_cast<size_t>(blocks) * g.n * sizeof(uint32_t) : 0;
+  if (acc_need > r.fast_acc_bytes) {
+    if (r.fast_acc) cudaFree(r.fast_acc);
+    r.fast_acc = nullptr;
+    r.fast_acc_bytes = 0;
+    SMG_CUDA(cudaMalloc(&r.fast_acc, acc_need));
+    r.fast_acc_bytes = acc_need;
+  }
+  if (dense_need > r.fast_dense_bytes) {
+    if (r.fast_dense) cudaFree(r.fast_dense);
+    r.fast_dense = nullptr;
+    r.fast_dense_bytes = 0;
+    SMG_CUDA(cudaMalloc(&r.fast_dense, dense_need));
+    SMG_CUDA(cudaMemsetAsync(r.fast_dense, 0, dense_need, st));
+    r.fast_dense_bytes = dense_need;
+  }
+  const size_t need = static_cast<size_t>(blocks) * (kFastThreads / 32) * words * sizeof(uint32_t);
+  if (need > r.fast_scratch_bytes) {
+    if (r.fast_scratch) cudaFree(r.fast_scratch);
+    r.fast_scratch = nullptr;
+    r.fast_scratch_bytes = 0;
+    SMG_CUDA(cudaMalloc(&r.fast_scratch, need));
+    SMG_CUDA(cudaMemsetAsync(r.fast_scratch, 0, need, st));
+    r.fast_scratch_bytes = need;
+  }
+  FastArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.off = r.off;
+  a.adj = r.adj;
+  a.src = r.src;
+  a.n = g.n;
+  a.slots = g.slots;
+  a.root_lo = L.root_lo;
+  a.root_hi = L.root_hi;
+  a.num_shards = L.num_shards;
+  if (L.num_shards > 1) {
+    int mrc = ensure_shard_map(g, r, L.num_shards, plan.parent[1] == 0 ? 1 : 0);
+    if (mrc) return mrc;
+    a.map_begin = r.map_dev + static_cast<size_t>(L.shard) * (2 * kShardSplit + 1);
+    a.map_pref = a.map_begin + kShardSplit;
+    a.map_k = kShardSplit;
+  }
+  a.t = r.tix;
+  a.scratch = r.fast_scratch;
+  a.scratch_words = words;
+  a.dmax = g.max_degree;
+  a.next_chunk = &r.ctr->next_chunk;
+  a.next2 = &r.ctr->heavy_next;
+  a.acc0 = r.fast_acc;
+  a.acc1 = r.fast_acc ? r.fast_acc + g.slots : nullptr;
+  a.acc2 = r.fast_acc ? r.fast_acc + (fast_slot_arrays(kind) - 1) * g.slots : nullptr;
+  a.dense = r.fast_dense;
+  a.count = &r.ctr->count;
+  a.units = &r.ctr->units;
+  a.overflow = &r.ctr->overflow;
+  SMG_CUDA(cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st));
+  SMG_CUDA(cudaEventRecord(r.ev0, st));
+  if (g.slots && fast_launch(kind, a, blocks, st)) return fail(SMG_EIO, "folded kernel launch failed");
+  SMG_CUDA(cudaGetLastError());
+  SMG_CUDA(cudaEventRecord(r.ev1, st));
+  SMG_CUDA(cudaMemcpyAsync(r.host_ctr, r.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  return SMG_OK;
+}
+
+// The folded kernel for this call, or kFastNone.
+int fast_for(const smg_plan& plan, uint32_t flags) {
+  if (!g_fast || (flags & (SMG_METER | SMG_GENERIC))) return kFastNone;
+  return fast_kind(plan);
+}
+
 int enqueue(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
   SMG_CUDA(cudaSetDevice(r.device));
   if (prog.batch && prog.depth == 4) {
@@ -2712,7 +2818,8 @@ int smg_plan_describe(const smg_plan* plan, char* buf, size_t cap) {
   s += ",\"batch\":" + std::to_string(pr.batch) + ",\"batch_diff\":" + std::to_string(pr.batch_diff) +
        ",\"batch_yltx\":" + std::to_string(pr.batch_yltx) +
        ",\"batch_fixed_bound\":" + std::to_string(pr.batch_fixed_bound) +
-       ",\"clique\":" + std::to_string(pr.clique) + ",\"parent\":[";
+       ",\"clique\":" + std::to_string(pr.clique) + ",\"fast\":" + std::to_string(fast_kind(*plan)) +
+       ",\"parent\":[";
   for (int i = 0; i < pr.depth; ++i) s += (i ? "," : "") + std::to_string(pr.parent[i]);
   s += "]}";
   if (s.size() + 1 > cap) return fail(SMG_EINPUT, "buffer too small");
@@ -2730,6 +2837,10 @@ void smg_graph_destroy(smg_graph* g) {
     park_work(*r);  // per-warp scratch, queues and bitmaps go to the device's pool
     if (r->ctr) cudaFree(r->ctr);
     if (r->map_dev) cudaFree(r->map_dev);
+    tindex_free(&r->tix);
+    if (r->fast_scratch) cudaFree(r->fast_scratch);
+    if (r->fast_acc) cudaFree(r->fast_acc);
+    if (r->fast_dense) cudaFree(r->fast_dense);
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
     if (r->ev0) cudaEventDestroy(r->ev0);
     if (r->ev1) cudaEventDestroy(r->ev1);
@@ -3011,7 +3122,10 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
   L.meter_roots = (shard == 0);
   L.shard = shard;
   L.num_shards = num_shards;
-  rc = enqueue(*g, r, prog, L);
+  {
+    const int fk = fast_for(*plan, flags);
+    rc = fk ? enqueue_fast(*g, r, fk, *plan, L) : enqueue(*g, r, prog, L);
+  }
   if (rc) return rc;
   bool ovf = false;
   rc = finish(r, &out->count, &out->elements, &out->units, &ovf, &out->kernel_ms);
@@ -3155,7 +3269,10 @@ int smg_count_range(const smg_graph* g, const smg_plan* plan, int replica, uint3
   L.root_lo = lo;
   L.root_hi = hi;
   L.meter_roots = true;
-  rc = enqueue(*g, r, prog, L);
+  {
+    const int fk = fast_for(*plan, flags);
+    rc = fk ? enqueue_fast(*g, r, fk, *plan, L) : enqueue(*g, r, prog, L);
+  }
   if (rc) return rc;
   bool ovf = false;
   rc = finish(r, &out->count, &out->elements, &out->units, &ovf, &out->kernel_ms);
@@ -3188,7 +3305,8 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
     L.meter_roots = (d == 0);
     L.shard = d;
     L.num_shards = num_gpus;
-    rc = enqueue(*g, *g->reps[d], prog, L);
+    const int fk = fast_for(*plan, flags);
+    rc = fk ? enqueue_fast(*g, *g->reps[d], fk, *plan, L) : enqueue(*g, *g->reps[d], prog, L);
     if (rc) {
       // devices 0..d-1 are still counting into their Counters: drain them
       // before the replica locks are released

@@ -1,0 +1,81 @@
+// tindex.hpp -- triangle index and the folded (closed-form) unit counts of the
+// star-shaped plans (see tindex.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/symmine_gpu.h"
+
+namespace smg {
+
+// Per-slot common-neighbour lists of a device CSR.  For slot e = (u, v) (v in
+// N(u)), T(e) lists the positions p in N(u) (0 <= p < deg u) with
+// adj[off[u] + p] in N(v), ascending (= ascending ids).  T(e) is the row of v
+// in the local graph G[N(u)] -- the ego network of u -- in local ids.
+struct TIndex {
+  uint64_t slots = 0;
+  uint64_t entries = 0;                   // sum of tri = 6 x #triangles
+  unsigned long long* rev = nullptr;      // slots: index of the reverse slot (v, u)
+  uint32_t* tri = nullptr;                // slots: |N(u) & N(v)|
+  unsigned long long* toff = nullptr;     // slots + 1: T-list offsets
+  uint32_t* tent = nullptr;               // entries: positions in N(u)
+  unsigned long long* lowpref = nullptr;  // slots: sum over earlier slots f of u of |T(f) & [0, pos f)|
+  uint32_t* k4 = nullptr;                 // entries: |T(u, x) & T(u, w)| for entry w of T(u, x)
+  bool has_low = false, has_k4 = false;
+};
+
+// Builds the parts that are missing (the lists always; lowpref / k4 on
+// request).  Returns 0, or 1 with *err set on a CUDA error (out of memory).
+int tindex_build(TIndex* t, const unsigned long long* off, const uint32_t* adj, const uint32_t* src,
+                 uint64_t n, uint64_t slots, int num_sms, cudaStream_t st, bool want_low, bool want_k4,
+                 std::string* err);
+void tindex_free(TIndex* t);
+
+// Plans whose deeper levels all lie in the neighbourhood of v1 and whose
+// leaves fold into closed forms over the ego network of v1 (tindex.cu).
+enum FastKind {
+  kFastNone = 0, kFastStar4 = 1, kFastTailedDiamondA = 2, kFastHouse = 3, kFastTailedDiamondB = 4,
+  kFastTailedTriangle = 5, kFastDiamond = 6, kFastPath4 = 7, kFastRectangle = 8, kFastRectangleMotif = 9
+};
+int fast_kind(const smg_plan& p);
+
+struct FastArgs {
+  const unsigned long long* off;
+  const uint32_t* adj;
+  const uint32_t* src;
+  uint64_t n, slots;
+  uint32_t root_lo, root_hi;           // units (v0, v1) with v0 in [root_lo, root_hi)
+  uint32_t num_shards;                 // > 1: shard map below
+  const unsigned long long* map_begin;
+  const unsigned long long* map_pref;
+  uint32_t map_k;
+  TIndex t;
+  uint32_t* scratch;                   // per warp: scratch_words words (zero between units)
+  uint64_t scratch_words;
+  uint64_t dmax;                       // max degree
+  // two-center kinds (house, tailed diamond b): per-slot accumulators and a
+  // dense per-CTA codegree table of n words (zero between centers)
+  unsigned long long* acc0;            // slots
+  unsigned long long* acc1;            // slots
+  unsigned long long* acc2;            // slots
+  uint32_t* dense;                     // blocks x n
+  unsigned long long* next2;           // second queue cursor (zeroed by the caller)
+  unsigned long long* next_chunk;      // queue cursor (zeroed by the caller)
+  unsigned long long* count;           // checked uint64 sum
+  unsigned long long* units;
+  unsigned int* overflow;
+};
+
+// Scratch words per warp that a kind needs for max degree dmax; per-slot
+// accumulator arrays (0..3) and whether it needs the dense per-CTA tables.
+uint64_t fast_scratch_words(int kind, uint64_t dmax);
+int fast_slot_arrays(int kind);
+bool fast_dense(int kind);
+// Blocks x 256 threads, persistent.
+int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st);
+constexpr int kFastThreads = 256;
+
+}  // namespace smg

@@ -46,15 +46,20 @@ def _plan(plan) -> Plan:
     raise N.InputError("plan must be a Plan or plan JSON")
 
 
-def count_result(graph: Graph, plan, gpus: int = 1, meter: bool = False) -> CountResult:
-    """count_instances(g, plan, workers=gpus) on `gpus` B200s (one process)."""
+def _flags(meter: bool, generic: bool) -> int:
+    return (N.SMG_METER if meter else 0) | (N.SMG_GENERIC if generic else 0)
+
+
+def count_result(graph: Graph, plan, gpus: int = 1, meter: bool = False, generic: bool = False) -> CountResult:
+    """count_instances(g, plan, workers=gpus) on `gpus` B200s (one process).
+    generic=True forces the plan executor where a folded kernel exists."""
     p = _plan(plan)
     gpus = max(1, int(gpus))  # workers == 0 -> 1 (engine.cpp:146)
     lib = N.gpu_lib()
     h = graph.device_handle(tuple(range(gpus)))
     sp = p.to_smg()
     r = N.SmgResult()
-    N.check_gpu(lib.smg_count(h, ctypes.byref(sp), gpus, N.SMG_METER if meter else 0, ctypes.byref(r)))
+    N.check_gpu(lib.smg_count(h, ctypes.byref(sp), gpus, _flags(meter, generic), ctypes.byref(r)))
     return _result(r, gpus)
 
 
@@ -74,26 +79,27 @@ def motif_counts(graph: Graph, k: int, gpus: int = 1) -> list[dict]:
     return out
 
 
-def count_range(graph: Graph, plan, lo: int, hi: int, device: int = 0, meter: bool = False) -> CountResult:
+def count_range(graph: Graph, plan, lo: int, hi: int, device: int = 0, meter: bool = False,
+                generic: bool = False) -> CountResult:
     p = _plan(plan)
     lib = N.gpu_lib()
     h = graph.device_handle((device,))
     sp = p.to_smg()
     r = N.SmgResult()
-    N.check_gpu(lib.smg_count_range(h, ctypes.byref(sp), 0, lo, hi, N.SMG_METER if meter else 0,
+    N.check_gpu(lib.smg_count_range(h, ctypes.byref(sp), 0, lo, hi, _flags(meter, generic),
                                     ctypes.byref(r)))
     return _result(r, 1)
 
 
 def count_shard(graph: Graph, plan, shard: int, num_shards: int, device: int = 0,
-                meter: bool = False) -> CountResult:
+                meter: bool = False, generic: bool = False) -> CountResult:
     p = _plan(plan)
     lib = N.gpu_lib()
     h = graph.device_handle((device,))
     sp = p.to_smg()
     r = N.SmgResult()
     N.check_gpu(lib.smg_count_shard(h, ctypes.byref(sp), 0, shard, num_shards,
-                                    N.SMG_METER if meter else 0, ctypes.byref(r)))
+                                    _flags(meter, generic), ctypes.byref(r)))
     return _result(r, 1)
 
 

@@ -5,9 +5,11 @@
 // symmine::gpu::count_instances (B200).  Built by `make -C oracle adapter`
 // against /root/reference headers; run by tests/test_gpu.py.
 #include <cstdio>
+#include <optional>
 #include <random>
 
 #include "symmine/cost_model.hpp"
+#include "symmine/pattern.hpp"
 #include "symmine/engine.hpp"
 #include "symmine/error.hpp"
 #include "symmine_gpu.hpp"
@@ -48,6 +50,49 @@ int main() {
     std::printf("InputError as expected: %s\n", e.what());
   }
   gpu::release(g);
+
+  // A loop-scoped Graph that lands where a released one lived must not reuse
+  // the stale device replica (the cache checks a content fingerprint).
+  {
+    std::optional<Graph> slot;
+    const Plan tri = compile_plan(named_pattern("triangle"), {0, 1, 2}, {-1, 0, 1});
+    for (int round = 0; round < 3; ++round) {
+      std::vector<std::pair<VertexId, VertexId>> es;
+      const VertexId k = 20 + 5 * round;  // K_k: C(k,3) triangles
+      for (VertexId i = 0; i < k; ++i)
+        for (VertexId j = i + 1; j < k; ++j) es.emplace_back(i, j);
+      slot.emplace(Graph::from_edges(k, es));
+      const uint64_t want = uint64_t(k) * (k - 1) * (k - 2) / 6;
+      const uint64_t got = gpu::count_instances(*slot, tri, 1).count;
+      std::printf("K_%u triangles: gpu=%llu want=%llu\n", k, (unsigned long long)got, (unsigned long long)want);
+      if (got != want) ++bad;
+      slot.reset();  // destroyed without release(): the next Graph may reuse the address
+    }
+  }
+
+  // A real device overflow: induced 3-stars (motif star4 plan, as motif_counts
+  // compiles it, engine.cpp:193-205) in a star with 5,000,000 leaves number
+  // C(5e6, 3) > 2^64 -> CountOverflowError, like checked_add (engine.cpp:13-19).
+  {
+    const VertexId leaves = 5000000;
+    std::vector<std::pair<VertexId, VertexId>> es;
+    es.reserve(leaves);
+    for (VertexId i = 1; i <= leaves; ++i) es.emplace_back(0, i);
+    const Graph star = Graph::from_edges(leaves + 1, es);
+    for (Pattern& p : connected_patterns(4)) {
+      if (pattern_display_name(p) != "star4") continue;
+      const SelectedSchedule ss = select_schedule(p, {});
+      const Plan plan = compile_plan(p, ss.choice.schedule, ss.choice.restrictions);
+      try {
+        const CountResult r = gpu::count_instances(star, plan, 1);
+        std::printf("star4 on the 5M-leaf star: no overflow (count %llu)\n", (unsigned long long)r.count);
+        ++bad;
+      } catch (const CountOverflowError& e) {
+        std::printf("CountOverflowError as expected: %s\n", e.what());
+      }
+    }
+    gpu::release(star);
+  }
   std::printf(bad ? "FAILED\n" : "OK\n");
   return bad ? 1 : 0;
 }

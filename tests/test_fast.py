@@ -1,0 +1,85 @@
+"""The folded closed-form kernels (csrc/tindex.cu) against the reference.
+
+For the star-shaped plans (every level >= 2 inside N(v1)) the engine counts a
+unit (v0, v1) in the ego network of v1 from the triangle index instead of
+enumerating the last two loops.  The result must be the plan's own per-unit
+count: per-root counts equal the reference's Executor::count_range
+(engine.cpp:36-43) on the corpus, totals equal the generic executor and the C
+restatement on mid-size hub-heavy graphs, shards partition the count."""
+from __future__ import annotations
+
+import ctypes
+import json
+
+import numpy as np
+import pytest
+
+from common import er_graph
+from paper_1911_12877_b200 import Graph, configs, count_range, count_result, count_shard, named_plan
+from paper_1911_12877_b200 import _native as N
+from paper_1911_12877_b200.plan import motif_plans
+
+FOLDED = {"star4": 1, "tailed_diamond_a": 2, "house": 3, "tailed_diamond_b": 4, "tailed_triangle": 5,
+          "diamond": 6, "path4": 7, "rectangle": 8, "rectangle_motif": 9}
+MOTIF_KIND = {"star4": 1, "tailed_triangle": 5, "diamond": 6, "path4": 7, "rectangle": 9}
+
+
+def folded_plans():
+    motifs = {r["name"]: r["plan"] for r in motif_plans(4)}
+    return {"star4": motifs["star4"], "tailed_diamond_a": named_plan("tailed_diamond_a"),
+            "house": named_plan("house"), "tailed_diamond_b": named_plan("tailed_diamond_b"),
+            "tailed_triangle": motifs["tailed_triangle"], "diamond": motifs["diamond"], "path4": motifs["path4"],
+            "rectangle": named_plan("rectangle"), "rectangle_motif": motifs["rectangle"]}
+
+
+def describe(plan):
+    sp = plan.to_smg()
+    buf = ctypes.create_string_buffer(1 << 16)
+    N.check_gpu(N.gpu_lib().smg_plan_describe(ctypes.byref(sp), buf, 1 << 16))
+    return json.loads(buf.value.decode())
+
+
+def test_folded_kinds_are_recognised():
+    """Host-only: which plans lower to a folded kernel (fast_kind)."""
+    for name, plan in folded_plans().items():
+        assert describe(plan)["fast"] == FOLDED[name], name
+        assert describe(plan.with_options(False, True))["fast"] == 0  # restrictions off: generic
+    for name in ("triangle", "pentagon", "clique:4", "clique:5"):
+        assert describe(named_plan(name))["fast"] == 0, name
+    for r in motif_plans(4):
+        assert describe(r["plan"])["fast"] == MOTIF_KIND.get(r["name"], 0), r["name"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p,seed", [(30, 0.3, 1), (40, 0.5, 2), (25, 0.7, 3), (60, 0.15, 4), (80, 0.08, 5)])
+def test_folded_per_root_vs_reference(reference, n, p, seed):
+    g = Graph.from_edges(*er_graph(n, p, seed))
+    rg = reference.graph_from_csr(g.offsets, g.adjacency)
+    for name, plan in folded_plans().items():
+        want, _ = rg.count_roots(plan.to_json(), np.arange(g.n, dtype=np.uint32), 4)
+        got = [count_range(g, plan, v, v + 1).count for v in range(g.n)]
+        assert got == [int(x) for x in want], name
+        assert count_result(g, plan).count == int(want.sum())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", [configs.GraphSpec("rmat", (12, 8, 0.57, 0.19, 0.19), 11),
+                                  configs.GraphSpec("rmat", (14, 16, 0.57, 0.19, 0.19), 21),
+                                  configs.GraphSpec("chung_lu", (6000, 60000, 2.1, 600.0), 12),
+                                  configs.GraphSpec("chung_lu", (20000, 400000, 2.3, 2000.0), 22),
+                                  configs.GraphSpec("er", (3000, 30000), 13)],
+                         ids=lambda s: s.tag)
+def test_folded_vs_generic_and_oracle(spec, port):
+    g = configs.load(spec)
+    for name, plan in folded_plans().items():
+        fast = count_result(g, plan)
+        gen = count_result(g, plan, generic=True)
+        assert fast.count == gen.count, name
+        assert fast.units == gen.units, name
+        if g.n <= 6000:
+            c, _ = port.count(g.offsets, g.adjacency, plan.to_smg(), threads=8)
+            assert fast.count == c, name
+        parts = [count_shard(g, plan, i, 3) for i in range(3)]
+        assert sum(r.count for r in parts) == fast.count
+        lo, hi = g.n // 3, g.n // 2
+        assert count_range(g, plan, lo, hi).count == count_range(g, plan, lo, hi, generic=True).count
