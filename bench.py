@@ -303,6 +303,7 @@ def our_arm(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / transport lines on stderr
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():

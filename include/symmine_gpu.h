@@ -52,6 +52,11 @@ extern "C" {
  * for the plan (the folded kernels, tindex.cu, never meter E: SMG_METER also
  * selects the generic executor).  For A/B parity checks. */
 #define SMG_GENERIC 2u
+/* Root-range calls (smg_count_range) of the two-centre folded kinds (house,
+ * tailed diamond b, path4, rectangle) run the generic executor unless this
+ * flag asks for the folded per-unit passes (they sweep the whole graph once,
+ * then serve later ranges from cached per-unit values). */
+#define SMG_FOLDED_RANGE 4u
 
 /*
  * One compiled plan, the POD image of symmine::Plan (plan.hpp:25-37) as
@@ -82,6 +87,12 @@ typedef struct smg_result {
   uint64_t units;                  /* level-1 partial embeddings (v0,v1) processed  */
   double wall_ms;                  /* host wall time of the call                    */
   double kernel_ms;                /* device time of the counting kernels (max/GPU) */
+  /* High 64 bits (two's complement) of a shard's signed partial: the folded
+   * full-count kernels (house, tailed diamonds) split closed-form terms so a
+   * single shard's share may fall outside [0, 2^64); the shares still sum
+   * exactly to the count.  Always 0 for smg_count / smg_count_range and for
+   * every other plan. */
+  int64_t count_hi;
 } smg_result;
 
 typedef struct smg_graph smg_graph;

@@ -24,6 +24,7 @@ MAX_GPUS = 8
 
 SMG_OK, SMG_EIO, SMG_EINPUT, SMG_EOVERFLOW = 0, 1, 2, 3
 SMG_GENERIC = 2  # flag: plan executor even where a folded kernel exists
+SMG_FOLDED_RANGE = 4  # flag: folded passes for root ranges of the two-centre kinds
 SMG_PLAN_USE_BOUNDS = 1
 SMG_PLAN_USE_RESTRICTIONS = 2
 SMG_METER = 1
@@ -60,6 +61,7 @@ class SmgResult(ctypes.Structure):
         ("units", ctypes.c_uint64),
         ("wall_ms", ctypes.c_double),
         ("kernel_ms", ctypes.c_double),
+        ("count_hi", ctypes.c_int64),
     ]
 
 
@@ -118,7 +120,7 @@ def gpu_lib():
                    ctypes.c_uint32, ctypes.POINTER(SmgResult)])
             _bind(lib, "smg_shard_bounds", ctypes.c_int,
                   [_P, ctypes.c_int, ctypes.c_uint32, ctypes.c_int, _U64P])
-            if lib.smg_abi_version() != 1:
+            if lib.smg_abi_version() != 2:
                 raise IoError("libsymmine_gpu.so ABI version mismatch; rebuild")
             _gpu = lib
         return _gpu

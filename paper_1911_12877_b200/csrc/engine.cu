@@ -2312,6 +2312,16 @@ struct Replica {
   size_t fast_scratch_bytes = 0;
   unsigned long long* fast_acc = nullptr;              // per-slot accumulators (two-center kinds)
   size_t fast_acc_bytes = 0;
+  int fast_acc_kind = 0;                               // kind whose accumulators fast_acc holds
+  // folded full-count mode: per-CTA signed partials, global closed-form terms
+  unsigned long long* part_dev = nullptr;
+  unsigned long long* part_host = nullptr;             // pinned
+  size_t part_words = 0;
+  bool k4pairs_valid = false, k5_valid = false;
+  unsigned long long k4pairs = 0, k5 = 0;              // cached: the graph is immutable
+  int post_kind = 0;                                   // > 0: finish() combines the partials
+  unsigned post_blocks = 0;
+  __int128 post_global = 0;
   uint32_t* fast_dense = nullptr;                      // per-CTA dense codegree tables
   size_t fast_dense_bytes = 0;
   std::mutex mu;
@@ -2619,6 +2629,47 @@ int enqueue_t(const smg_graph& g, Replica& r, const Program& prog, const Launch&
   return SMG_OK;
 }
 
+int enqueue(const smg_graph& g, Replica& r, const Program& prog, const Launch& L);
+int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* ovf, double* ms,
+           int64_t* count_hi = nullptr);
+
+// Number of 5-cliques (clique plan, v0 > v1 > ... > v4: each K5 once) through
+// the generic executor's clique-local path; a closed-form term of the folded
+// full counts.  Cached on the replica.  Caller holds r.mu.
+int replica_k5(const smg_graph& g, Replica& r, unsigned long long* out) {
+  if (!r.k5_valid) {
+    smg_plan p;
+    std::memset(&p, 0, sizeof(p));
+    p.depth = 5;
+    for (int i = 0; i < SMG_MAX_LEVELS; ++i) p.parent[i] = -1;
+    for (int i = 1; i < 5; ++i) {
+      p.isect_mask[i] = static_cast<uint8_t>((1u << i) - 1u);
+      p.parent[i] = static_cast<int8_t>(i - 1);
+    }
+    p.flags = SMG_PLAN_USE_BOUNDS | SMG_PLAN_USE_RESTRICTIONS;
+    Program prog;
+    const std::string err = compile_program(p, &prog);
+    if (!err.empty()) return fail(SMG_EIO, "internal clique plan: " + err);
+    Launch L;
+    L.unit_begin = 0;
+    L.unit_end = g.slots;
+    L.root_lo = 0;
+    L.root_hi = static_cast<uint32_t>(g.n);
+    int rc = enqueue(g, r, prog, L);
+    if (rc) return rc;
+    uint64_t c = 0, el = 0, u = 0;
+    bool ovf = false;
+    double ms = 0;
+    rc = finish(r, &c, &el, &u, &ovf, &ms);
+    if (rc) return rc;
+    if (ovf) return fail(SMG_EOVERFLOW, "5-clique count exceeds 64 bits");
+    r.k5 = c;
+    r.k5_valid = true;
+  }
+  *out = r.k5;
+  return SMG_OK;
+}
+
 // The folded closed-form path (tindex.cu) for plans fast_kind() recognises:
 // builds the triangle index on first use (cached on the replica), then one
 // persistent kernel over the level-1 unit slots.  Same Counters, events and
@@ -2628,8 +2679,10 @@ int enqueue_fast(const smg_graph& g, Replica& r, int kind, const smg_plan& plan,
   cudaStream_t st = r.active();
   std::string err;
   const auto tb0 = std::chrono::steady_clock::now();
+  const bool full = L.root_lo == 0 && L.root_hi == g.n;
+  const bool fullmode = full && fast_has_full(kind);
   if (tindex_build(&r.tix, r.off, r.adj, r.src, g.n, g.slots, r.num_sms, st, kind == kFastStar4,
-                   kind == kFastTailedDiamondA, &err)) {
+                   kind == kFastTailedDiamondA || fullmode, &err)) {
     tindex_free(&r.tix);
     return fail(SMG_EIO, "triangle index: " + err);
   }
@@ -2640,13 +2693,20 @@ int enqueue_fast(const smg_graph& g, Replica& r, int kind, const smg_plan& plan,
   const bool dense = fast_dense(kind);
   const unsigned blocks = static_cast<unsigned>(r.num_sms) * (dense ? 2 : 4);
   const uint64_t words = fast_scratch_words(kind, g.max_degree);
-  // per-slot accumulators and dense per-CTA codegree tables (two-center kinds)
-  const size_t acc_need = static_cast<size_t>(fast_slot_arrays(kind)) * std::max<uint64_t>(g.slots, 1) * 8;
+  // per-slot accumulators and dense per-CTA codegree tables (two-center kinds;
+  // the rectangle kinds use an accumulator only for root-range calls).  The
+  // accumulators of a completed pass stay valid (the graph is immutable), so
+  // later root-range calls of the same kind only run the combine.
+  const bool rect = kind == kFastRectangle || kind == kFastRectangleMotif;
+  const bool arrays = fast_slot_arrays(kind) > 0 && !(rect && full) && !fullmode;
+  const bool combine_only = arrays && !full && r.fast_acc_kind == kind;
+  const size_t acc_need = arrays ? static_cast<size_t>(fast_slot_arrays(kind)) * std::max<uint64_t>(g.slots, 1) * 8 : 0;
   const size_t dense_need = dense ? static_cast<size_t>(blocks) * g.n * sizeof(uint32_t) : 0;
   if (acc_need > r.fast_acc_bytes) {
     if (r.fast_acc) cudaFree(r.fast_acc);
     r.fast_acc = nullptr;
     r.fast_acc_bytes = 0;
+    r.fast_acc_kind = 0;
     SMG_CUDA(cudaMalloc(&r.fast_acc, acc_need));
     r.fast_acc_bytes = acc_need;
   }
@@ -2676,6 +2736,9 @@ int enqueue_fast(const smg_graph& g, Replica& r, int kind, const smg_plan& plan,
   a.slots = g.slots;
   a.root_lo = L.root_lo;
   a.root_hi = L.root_hi;
+  a.e_lo = full ? 0 : L.unit_begin;
+  a.e_hi = full ? g.slots : L.unit_end;
+  a.via_rev = (!full && fast_center_v1(kind)) ? 1 : 0;
   a.num_shards = L.num_shards;
   if (L.num_shards > 1) {
     int mrc = ensure_shard_map(g, r, L.num_shards, plan.parent[1] == 0 ? 1 : 0);
@@ -2690,26 +2753,67 @@ int enqueue_fast(const smg_graph& g, Replica& r, int kind, const smg_plan& plan,
   a.dmax = g.max_degree;
   a.next_chunk = &r.ctr->next_chunk;
   a.next2 = &r.ctr->heavy_next;
-  a.acc0 = r.fast_acc;
-  a.acc1 = r.fast_acc ? r.fast_acc + g.slots : nullptr;
-  a.acc2 = r.fast_acc ? r.fast_acc + (fast_slot_arrays(kind) - 1) * g.slots : nullptr;
+  a.acc0 = arrays ? r.fast_acc : nullptr;
+  a.acc1 = arrays ? r.fast_acc + g.slots : nullptr;
+  a.acc2 = arrays ? r.fast_acc + (fast_slot_arrays(kind) - 1) * g.slots : nullptr;
   a.dense = r.fast_dense;
   a.count = &r.ctr->count;
   a.units = &r.ctr->units;
   a.overflow = &r.ctr->overflow;
+  r.post_kind = 0;
+  if (fullmode) {
+    // closed-form terms (shard 0 carries them): sum_entries k4(k4-1) and K5
+    __int128 global = 0;
+    if (L.shard == 0) {
+      if (!r.k4pairs_valid) {
+        if (tindex_k4_pairs(r.tix, r.num_sms, st, &r.k4pairs, &err)) return fail(SMG_EIO, err);
+        r.k4pairs_valid = true;
+      }
+      unsigned long long k5 = 0;
+      int krc = replica_k5(g, r, &k5);
+      if (krc) return krc;
+      const __int128 half = static_cast<__int128>(r.k4pairs / 2), k5x60 = static_cast<__int128>(k5) * 60;
+      global = k5x60 - half;  // house: -k4p/2 + 60 K5 (with ego/2); tdb, tda: -(k4p/2 - 60 K5)
+    }
+    const size_t words = 4 * static_cast<size_t>(blocks);
+    if (words > r.part_words) {
+      if (r.part_dev) cudaFree(r.part_dev);
+      if (r.part_host) cudaFreeHost(r.part_host);
+      r.part_dev = nullptr;
+      r.part_host = nullptr;
+      r.part_words = 0;
+      SMG_CUDA(cudaMalloc(&r.part_dev, words * sizeof(unsigned long long)));
+      SMG_CUDA(cudaMallocHost(&r.part_host, words * sizeof(unsigned long long)));
+      r.part_words = words;
+    }
+    a.part = r.part_dev;
+    r.post_global = global;
+    r.post_blocks = blocks;
+  }
   SMG_CUDA(cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st));
   SMG_CUDA(cudaEventRecord(r.ev0, st));
-  if (g.slots && fast_launch(kind, a, blocks, st)) return fail(SMG_EIO, "folded kernel launch failed");
+  if (fullmode) {
+    if (kind != kFastTailedDiamondA) SMG_CUDA(cudaMemsetAsync(r.part_dev, 0, r.part_words * 8, st));
+    if (g.slots && fast_launch_full(kind, a, blocks, st)) return fail(SMG_EIO, "folded kernel launch failed");
+    SMG_CUDA(cudaMemcpyAsync(r.part_host, r.part_dev, 4 * blocks * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st));
+    r.post_kind = kind;
+  } else if (g.slots && fast_launch(kind, a, blocks, st, combine_only)) {
+    return fail(SMG_EIO, "folded kernel launch failed");
+  }
+  if (arrays) r.fast_acc_kind = kind;
   SMG_CUDA(cudaGetLastError());
   SMG_CUDA(cudaEventRecord(r.ev1, st));
   SMG_CUDA(cudaMemcpyAsync(r.host_ctr, r.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   return SMG_OK;
 }
 
-// The folded kernel for this call, or kFastNone.
-int fast_for(const smg_plan& plan, uint32_t flags) {
+// The folded kernel for this call, or kFastNone.  range: a root-range call.
+int fast_for(const smg_plan& plan, uint32_t flags, bool range = false) {
   if (!g_fast || (flags & (SMG_METER | SMG_GENERIC))) return kFastNone;
-  return fast_kind(plan);
+  const int k = fast_kind(plan);
+  if (range && !(flags & SMG_FOLDED_RANGE) && (fast_dense(k) || fast_slot_arrays(k))) return kFastNone;
+  return k;
 }
 
 int enqueue(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
@@ -2728,7 +2832,11 @@ int enqueue(const smg_graph& g, Replica& r, const Program& prog, const Launch& L
                  : enqueue_t<false, false, kShapeGeneric>(g, r, prog, L);
 }
 
-int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* ovf, double* ms) {
+// count_hi (may be null): high 64 bits of a signed shard share (folded
+// full-count kinds); with count_hi == null a share outside [0, 2^64) is an
+// overflow.
+int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* ovf, double* ms,
+           int64_t* count_hi) {
   SMG_CUDA(cudaSetDevice(r.device));
   SMG_CUDA(cudaStreamSynchronize(r.active()));
   float t = 0.f;
@@ -2738,6 +2846,23 @@ int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* 
   *units = r.host_ctr->units;
   *ovf = r.host_ctr->overflow != 0;
   *ms = t;
+  if (count_hi) *count_hi = 0;
+  if (r.post_kind) {
+    // centre partials [0, B), ego partials [B, 2B) as (lo, hi) pairs
+    __int128 center = 0, ego = 0;
+    for (unsigned i = 0; i < 2 * r.post_blocks; ++i) {
+      const __int128 v = static_cast<__int128>(
+          (static_cast<unsigned __int128>(r.part_host[2 * i + 1]) << 64) | r.part_host[2 * i]);
+      (i < r.post_blocks ? center : ego) += v;
+    }
+    __int128 total = r.post_global;
+    if (r.post_kind == kFastTailedDiamondA) total += static_cast<__int128>(r.host_ctr->count);
+    else total += center + (r.post_kind == kFastHouse ? ego / 2 : ego);
+    r.post_kind = 0;
+    *count = static_cast<uint64_t>(total);
+    if (count_hi) *count_hi = static_cast<int64_t>(total >> 64);
+    else if (total < 0 || (total >> 64) != 0) *ovf = true;
+  }
   if (g_trace) {
     static const char* names[kTrCount] = {"units", "build_cycles", "batch_cycles", "batches",
                                           "batches_hashed", "stream_elems", "search_lists",
@@ -2768,7 +2893,7 @@ using namespace smg;
 
 extern "C" {
 
-int smg_abi_version(void) { return 1; }
+int smg_abi_version(void) { return 2; }
 
 const char* smg_last_error(void) { return g_last_error.c_str(); }
 
@@ -2841,6 +2966,8 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->fast_scratch) cudaFree(r->fast_scratch);
     if (r->fast_acc) cudaFree(r->fast_acc);
     if (r->fast_dense) cudaFree(r->fast_dense);
+    if (r->part_dev) cudaFree(r->part_dev);
+    if (r->part_host) cudaFreeHost(r->part_host);
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
     if (r->ev0) cudaEventDestroy(r->ev0);
     if (r->ev1) cudaEventDestroy(r->ev1);
@@ -3128,7 +3255,7 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
   }
   if (rc) return rc;
   bool ovf = false;
-  rc = finish(r, &out->count, &out->elements, &out->units, &ovf, &out->kernel_ms);
+  rc = finish(r, &out->count, &out->elements, &out->units, &ovf, &out->kernel_ms, &out->count_hi);
   if (rc) return rc;
   out->per_gpu[0] = out->count;
   out->wall_ms = now_ms() - t0;
@@ -3270,7 +3397,7 @@ int smg_count_range(const smg_graph* g, const smg_plan* plan, int replica, uint3
   L.root_hi = hi;
   L.meter_roots = true;
   {
-    const int fk = fast_for(*plan, flags);
+    const int fk = fast_for(*plan, flags, true);
     rc = fk ? enqueue_fast(*g, r, fk, *plan, L) : enqueue(*g, r, prog, L);
   }
   if (rc) return rc;
@@ -3322,21 +3449,23 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
     }
   }
   bool any_ovf = false;
+  __int128 total = 0;  // device shares may be signed (folded full-count kinds)
   for (unsigned d = 0; d < num_gpus; ++d) {
     uint64_t c = 0, el = 0, u = 0;
+    int64_t hi = 0;
     bool ovf = false;
     double ms = 0;
-    rc = finish(*g->reps[d], &c, &el, &u, &ovf, &ms);
+    rc = finish(*g->reps[d], &c, &el, &u, &ovf, &ms, &hi);
     if (rc) return rc;
     out->per_gpu[d] = c;
-    const uint64_t s = out->count + c;
-    if (s < out->count) any_ovf = true;
-    out->count = s;
+    total += static_cast<__int128>((static_cast<unsigned __int128>(static_cast<uint64_t>(hi)) << 64) | c);
     out->elements += el;
     out->units += u;
     out->kernel_ms = std::max(out->kernel_ms, ms);
     any_ovf |= ovf;
   }
+  if (total < 0 || (total >> 64) != 0) any_ovf = true;
+  out->count = static_cast<uint64_t>(total);
   out->wall_ms = now_ms() - t0;
   if (any_ovf) return fail(SMG_EOVERFLOW, "embedding count exceeds 64 bits");
   return SMG_OK;

@@ -266,8 +266,28 @@ __device__ __forceinline__ bool grab_chunk(const FastArgs& a, int lane, uint64_t
     while (a.map_pref[k + 1] <= chunk) ++k;
     g = a.map_begin[k] + (chunk - a.map_pref[k]);
   }
-  e0 = g * kSlotChunk;
-  return e0 < a.slots;
+  e0 = a.e_lo + g * kSlotChunk;
+  return e0 < a.e_hi;
+}
+
+__device__ __forceinline__ bool owns_chunk(const FastArgs& a, uint64_t q) {
+  if (a.num_shards <= 1) return true;
+  for (uint32_t k = 0; k < a.map_k; ++k) {
+    const ull b = a.map_begin[k], len = a.map_pref[k + 1] - a.map_pref[k];
+    if (q >= b && q < b + len) return true;
+  }
+  return false;
+}
+
+// a centre belongs to the shard that owns the chunk of its first slot
+__device__ __forceinline__ bool owns_center(const FastArgs& a, ull c) {
+  return a.num_shards <= 1 || owns_chunk(a, a.off[c] / kSlotChunk);
+}
+
+// The unit slot of walked slot e0 + lane (valid = inside the walk).
+__device__ __forceinline__ uint64_t unit_slot(const FastArgs& a, uint64_t ep, bool& valid) {
+  valid = ep < a.e_hi;
+  return valid ? (a.via_rev ? a.t.rev[ep] : ep) : 0;
 }
 
 __device__ __forceinline__ void checked_add(ull& acc, ull add, bool& ovf) {
@@ -313,8 +333,8 @@ __global__ void __launch_bounds__(kFastThreads) star4_kernel(const FastArgs a) {
   bool ovf = false;
   uint64_t e0;
   while (grab_chunk(a, lane, e0)) {
-    const uint64_t e = e0 + lane;
-    bool mine = e < a.slots;
+    bool mine;
+    const uint64_t e = unit_slot(a, e0 + lane, mine);
     uint32_t c = 0, p = 0;
     if (mine) {
       c = a.src[e];
@@ -387,8 +407,8 @@ __global__ void __launch_bounds__(kFastThreads) star_kernel(const FastArgs a) {
   bool ovf = false;
   uint64_t e0;
   while (grab_chunk(a, lane, e0)) {
-    const uint64_t e = e0 + lane;
-    bool mine = e < a.slots;
+    bool mine;
+    const uint64_t e = unit_slot(a, e0 + lane, mine);
     uint32_t c = 0, p = 0, v0 = 0;
     if (mine) {
       c = a.src[e];
@@ -429,6 +449,8 @@ __global__ void __launch_bounds__(kFastThreads) star_kernel(const FastArgs a) {
 }
 
 // Tailed diamond (a): one warp per unit with P = T(v1, v0) non-empty.
+// FULL: the S6 term is left out (summed in closed form by the caller).
+template <bool FULL>
 __global__ void __launch_bounds__(kFastThreads) tda_kernel(const FastArgs a) {
   const uint64_t dmax = a.dmax;
   __shared__ uint32_t ntouched[kFastThreads / 32];
@@ -441,8 +463,8 @@ __global__ void __launch_bounds__(kFastThreads) tda_kernel(const FastArgs a) {
   bool ovf = false;
   uint64_t e0;
   while (grab_chunk(a, lane, e0)) {
-    const uint64_t e = e0 + lane;
-    bool mine = e < a.slots;
+    bool mine;
+    const uint64_t e = unit_slot(a, e0 + lane, mine);
     uint32_t p = 0;
     if (mine) {
       p = a.adj[e];
@@ -453,7 +475,7 @@ __global__ void __launch_bounds__(kFastThreads) tda_kernel(const FastArgs a) {
     while (todo) {
       const int jl = __ffs(todo) - 1;
       todo &= todo - 1;
-      const uint64_t ue = e0 + jl;
+      const uint64_t ue = __shfl_sync(kAll, static_cast<ull>(e), jl);
       const uint32_t c = a.src[ue];
       const ull c0 = a.off[c];
       const uint32_t d1 = static_cast<uint32_t>(a.off[c + 1] - c0);
@@ -476,6 +498,7 @@ __global__ void __launch_bounds__(kFastThreads) tda_kernel(const FastArgs a) {
           const bool inP = (bm[x >> 5] >> (x & 31)) & 1u;
           if (inP) {
             ++c02;
+            if (FULL) continue;
             // w = x in P & T(v2): S6 += |T2[0,lb) & T(c,w) - P|
             const ull g = c0 + x;
             const uint32_t* Tg = a.t.tent + a.t.toff[g];
@@ -503,6 +526,7 @@ __global__ void __launch_bounds__(kFastThreads) tda_kernel(const FastArgs a) {
       ull pairs = 0, S3 = 0, S4 = 0;
       for (uint32_t z = lane; z < nt; z += 32) {
         const uint32_t x = touched[z];
+        touched[z] = 0u;  // every scratch word is zero between units (layouts differ per kind)
         const ull al = alpha[x];
         alpha[x] = 0u;
         pairs += al;
@@ -633,6 +657,7 @@ __global__ void __launch_bounds__(kFastThreads) house_eh_kernel(const FastArgs a
       const uint32_t nt = nt_sh[wib];
       for (uint32_t z = lane; z < nt; z += 32) {
         const uint32_t x = w.touched[z];
+        w.touched[z] = 0u;
         const ull al = w.t0[x];
         w.t0[x] = 0u;
         if (!bit(w.bm, x) && x != pa) {
@@ -740,6 +765,7 @@ __global__ void __launch_bounds__(kFastThreads) tdb_unit_kernel(const FastArgs a
       ull T2 = 0, T3 = 0;
       for (uint32_t z = lane; z < nt; z += 32) {
         const uint32_t x = w.touched[z];
+        w.touched[z] = 0u;
         const ull A = w.t0[x], B = w.t1[x];
         w.t0[x] = 0u;
         w.t1[x] = 0u;
@@ -807,7 +833,7 @@ __global__ void __launch_bounds__(kFastThreads) ego_w_kernel(const FastArgs a) {
         for (uint32_t k = lane; k < nb; k += 32) {
           const uint32_t x = Tb[k];
           if (!bit(w.bm, x)) {
-            if (x != pa) sum += KIND == kFastHouse ? w.t0[x] - 1u : w.t0[x];
+            if (x != pa) sum += KIND == kFastHouse ? static_cast<ull>(w.t0[x]) - 1 : static_cast<ull>(w.t0[x]);
           } else if (KIND == kFastHouse) {  // w = x in T(t,a) & T(t,b): |T(t,w) & T(t,b) - T(t,a) - {a}|
             const ull g = to + x;
             const uint32_t* Tg = a.t.tent + a.t.toff[g];
@@ -838,7 +864,10 @@ __global__ void __launch_bounds__(kFastThreads) ego_w_kernel(const FastArgs a) {
       }
       __syncwarp();
       const uint32_t nt = nt_sh[wib];
-      for (uint32_t z = lane; z < nt; z += 32) w.t0[w.touched[z]] = 0u;
+      for (uint32_t z = lane; z < nt; z += 32) {
+        w.t0[w.touched[z]] = 0u;
+        w.touched[z] = 0u;
+      }
       for (uint32_t j = lane; j < na; j += 32) w.bm[Ta[j] >> 5] = 0u;
       __syncwarp();
     }
@@ -849,7 +878,7 @@ __global__ void __launch_bounds__(kFastThreads) ego_w_kernel(const FastArgs a) {
 // order; the table holds the 2-hop scatter of N(c) & [0, u) when unit (c, u)
 // is evaluated (then u's own list is added).  NAMED: units u > c (c = v1);
 // motif: units u < c (c = v0).
-template <bool NAMED>
+template <bool NAMED, bool ARRAY>
 __global__ void __launch_bounds__(kFastThreads) rect_kernel(const FastArgs a) {
   __shared__ ull center_sh;
   __shared__ ull red_sh[kFastThreads / 32];
@@ -861,6 +890,7 @@ __global__ void __launch_bounds__(kFastThreads) rect_kernel(const FastArgs a) {
   for (;;) {
     const ull c = next_center(a, &center_sh);
     if (c >= a.n) break;
+    if (!ARRAY && !owns_center(a, c)) continue;  // shards split the centres
     const ull co = a.off[c];
     const uint32_t dc = static_cast<uint32_t>(a.off[c + 1] - co);
     // named: every neighbour is scattered, units are the u > c; motif: units
@@ -868,7 +898,10 @@ __global__ void __launch_bounds__(kFastThreads) rect_kernel(const FastArgs a) {
     const uint32_t steps = NAMED ? dc : lb32(a.adj + co, dc, static_cast<uint32_t>(c));
     for (uint32_t k = 0; k < steps; ++k) {
       const uint32_t u = a.adj[co + k];
-      const bool unit = (NAMED ? u > c : true) && (NAMED ? u : c) >= a.root_lo && (NAMED ? u : c) < a.root_hi;
+      // ARRAY: every unit's value goes to acc0[its slot (v0, v1)] (cached for
+      // root-range calls); else the units in the root range are summed here
+      const bool unit = (NAMED ? u > c : true) &&
+                        (ARRAY || ((NAMED ? u : c) >= a.root_lo && (NAMED ? u : c) < a.root_hi));
       if (unit) {
         const ull uo = a.off[u];
         const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
@@ -897,8 +930,12 @@ __global__ void __launch_bounds__(kFastThreads) rect_kernel(const FastArgs a) {
         if (threadIdx.x == 0) {
           ull v = 0;
           for (int w2 = 0; w2 < nw; ++w2) v += red_sh[w2];
-          checked_add(total, v, ovf);
-          ++units;
+          if (ARRAY) {
+            a.acc0[NAMED ? euc : co + k] = v;  // the unit's slot (v0, v1)
+          } else {
+            checked_add(total, v, ovf);
+            ++units;
+          }
         }
         for (uint32_t j = threadIdx.x; j < nT; j += blockDim.x) bm[T[j] >> 5] = 0u;
       }
@@ -937,23 +974,416 @@ __global__ void __launch_bounds__(kFastThreads) combine_kernel(const FastArgs a)
   bool ovf = false;
   uint64_t e0;
   while (grab_chunk(a, lane, e0)) {
-    const uint64_t e = e0 + lane;
-    bool mine = e < a.slots;
+    bool mine;
+    const uint64_t e = unit_slot(a, e0 + lane, mine);  // walks (v0, v1) slots directly
     uint32_t v0 = 0, v1 = 0;
     if (mine) {
       v0 = a.src[e];
       v1 = a.adj[e];
-      mine = v0 >= a.root_lo && v0 < a.root_hi && (KIND == kFastTailedDiamondB || v1 < v0);
+      mine = v0 >= a.root_lo && v0 < a.root_hi && (KIND == kFastTailedDiamondB || v1 < v0);  // rect/path4/house: v1 < v0
     }
     units += __popc(__ballot_sync(kAll, mine));
     if (mine) {
       const ull c = KIND == kFastHouse ? a.acc0[e] - a.acc1[e] - a.acc1[a.t.rev[e]] + a.acc2[e]
-                    : KIND == kFastPath4 ? a.acc0[e]
+                    : (KIND == kFastPath4 || KIND == kFastRectangle || KIND == kFastRectangleMotif) ? a.acc0[e]
                                          : a.acc0[e] + a.acc2[e];
       checked_add(cnt, c, ovf);
     }
   }
   flush(a, cnt, units, ovf, lane);
+}
+
+// Flattened pass over the entries of the index lists T(base + P[j]) for j in
+// [0, np): the warp's lanes take consecutive entries of their concatenation
+// (32 lists at a time, owner found by a shuffle search over the exclusive
+// scan), so short lists do not leave lanes idle.  aux(j) is a per-list word
+// carried to every entry; f(k, r, x, eidx, auxv): list j0 + k, entry r of it,
+// its value x, its index in tent.  All 32 lanes must call it; after(j, k) runs
+// on lane k for list j = j0 + k once its entries are done.
+template <class AUX, class F, class AFTER>
+__device__ __forceinline__ void flat_entries(const FastArgs& a, ull base, const uint32_t* P, uint32_t np, AUX aux,
+                                             F f, AFTER after) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t j0 = 0; j0 < np; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    uint32_t len = 0, av = 0;
+    ull to = 0;
+    if (j < np) {
+      const ull fs = base + P[j];
+      len = a.t.tri[fs];
+      to = a.t.toff[fs];
+      av = aux(j, fs, len, to);
+    }
+    uint32_t incl = len;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kAll, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const uint32_t tot = __shfl_sync(kAll, incl, 31), excl = incl - len;
+    for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
+      const uint32_t idx = t0 + lane;
+      int k = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t ex = __shfl_sync(kAll, excl, k + step);
+        if (ex <= idx) k += step;
+      }
+      const ull o_to = __shfl_sync(kAll, to, k);
+      const uint32_t o_ex = __shfl_sync(kAll, excl, k);
+      const uint32_t o_av = __shfl_sync(kAll, av, k);
+      if (idx < tot) {
+        const uint32_t r = idx - o_ex;
+        f(k, r, a.t.tent[o_to + r], o_to + r, o_av);
+      }
+    }
+    __syncwarp();
+    if (j < np) after(j, lane);
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------ full-count mode ---
+// For the whole root range the per-unit terms whose evaluation needs K4-level
+// merges are summed in closed form over the triangle index instead (checked
+// against per-unit evaluation in tests/test_fast.py):
+//   sum over units of S6 (tailed diamond a) = sum_entries C(k4, 2) - 60 K5
+//   sum over units of T5 (tailed diamond b) = 1/2 sum_entries k4 (k4 - 1) - 60 K5
+//   house: sum_units W = 1/2 [sum_{(t,a)} sum_{x not in N_L[a]} cl (cl - 1)
+//                             - sum_entries k4 (k4 - 1) + 120 K5]
+//          sum_units (H(v0,v1) + H(v1,v0)) = sum over all ordered slots of H
+// (K5 = number of 5-cliques, counted by the engine's clique-local path).  The
+// kernels below add each CTA's signed share to part[2 blockIdx] as 128 bits.
+typedef __int128 i128;
+
+
+__device__ __forceinline__ i128 warp_sum128(i128 v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    const ull lo = __shfl_xor_sync(kAll, static_cast<ull>(v), d);
+    const ull hi = __shfl_xor_sync(kAll, static_cast<ull>(v >> 64), d);
+    v += static_cast<i128>((static_cast<unsigned __int128>(hi) << 64) | lo);
+  }
+  return v;
+}
+
+// every thread calls it once, at the end; sums the block and stores its share
+__device__ void store_partial(const FastArgs& a, i128 v, ull units) {
+  __shared__ i128 red[kFastThreads / 32];
+  __shared__ ull ured[kFastThreads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  v = warp_sum128(v);
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) units += __shfl_xor_sync(kAll, units, d);
+  if (lane == 0) {
+    red[wib] = v;
+    ured[wib] = units;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = 0;
+    ull u = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      t += red[w];
+      u += ured[w];
+    }
+    a.part[2 * blockIdx.x] = static_cast<ull>(t);
+    a.part[2 * blockIdx.x + 1] = static_cast<ull>(t >> 64);
+    if (u) atomicAdd(a.units, u);
+  }
+}
+
+// house, centre a (dense c_a): sum over slots (a, b) of [b < a] |T| E(a, b) - H(a, b)
+__global__ void __launch_bounds__(kFastThreads) house_full_center_kernel(const FastArgs a) {
+  __shared__ ull center_sh;
+  __shared__ uint32_t nt_sh[kFastThreads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t* cnt = a.dense + static_cast<uint64_t>(blockIdx.x) * a.n;
+  const WarpScratch w = warp_scratch(a);
+  i128 acc = 0;
+  ull units = 0;
+  for (;;) {
+    const ull ca = next_center(a, &center_sh);
+    if (ca >= a.n) break;
+    const ull ao = a.off[ca];
+    const uint32_t da = static_cast<uint32_t>(a.off[ca + 1] - ao);
+    if (da == 0 || !owns_center(a, ca)) continue;
+    dense_scatter(a, cnt, ao, da, false);
+    __syncthreads();
+    for (uint32_t bb = wib; bb < da; bb += nw) {
+      const ull e = ao + bb;
+      const uint32_t b = a.adj[e];
+      const ull r = a.t.rev[e];
+      const ull bo = a.off[b];
+      const uint32_t db = static_cast<uint32_t>(a.off[b + 1] - bo);
+      const uint32_t pa = static_cast<uint32_t>(r - bo);
+      const uint32_t* Tba = a.t.tent + a.t.toff[r];
+      const uint32_t nT = a.t.tri[r];
+      const bool needE = b < ca;
+      if (lane == 0) {
+        nt_sh[wib] = 0;
+        if (needE) ++units;
+      }
+      for (uint32_t j = lane; j < nT; j += 32) atomicOr(&w.bm[Tba[j] >> 5], 1u << (Tba[j] & 31));
+      __syncwarp();
+      flat_entries(
+          a, bo, Tba, nT, [](uint32_t, ull, uint32_t, ull) { return 0u; },
+          [&](int, uint32_t, uint32_t x, ull, uint32_t) {
+            if (atomicAdd(&w.t0[x], 1u) == 0u) w.touched[atomicAdd(&nt_sh[wib], 1u)] = x;
+          },
+          [](uint32_t, int) {});
+      __syncwarp();
+      ull Esum = 0, sumA = 0, H = 0;
+      if (needE)
+        for (uint32_t x = lane; x < db; x += 32)
+          if (!bit(w.bm, x) && x != pa) Esum += cnt[a.adj[bo + x]];
+      const uint32_t nt = nt_sh[wib];
+      for (uint32_t z = lane; z < nt; z += 32) {
+        const uint32_t x = w.touched[z];
+        w.touched[z] = 0u;
+        const ull al = w.t0[x];
+        w.t0[x] = 0u;
+        if (!bit(w.bm, x) && x != pa) {
+          sumA += al;
+          H += al * (static_cast<ull>(cnt[a.adj[bo + x]]) - al - 1);
+        }
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < nT; j += 32) w.bm[Tba[j] >> 5] = 0u;
+      Esum = warp_sum(Esum);
+      sumA = warp_sum(sumA);
+      H = warp_sum(H);
+      __syncwarp();
+      if (lane == 0) {
+        if (needE) acc += static_cast<i128>(nT) * static_cast<i128>(Esum - sumA - static_cast<ull>(db - nT - 1));
+        acc -= static_cast<i128>(H);
+      }
+    }
+    __syncthreads();
+    dense_scatter(a, cnt, ao, da, true);
+  }
+  store_partial(a, acc, units);
+}
+
+// tailed diamond (b), centre v1 (dense c_v1): sum over its units of T1 - T2 + T3
+// (T1's |P & N(v2)| is the index's k4 of entry v1 in T(v0, v2)).
+__global__ void __launch_bounds__(kFastThreads) tdb_full_center_kernel(const FastArgs a) {
+  __shared__ ull center_sh;
+  __shared__ uint32_t nt_sh[kFastThreads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t* cnt = a.dense + static_cast<uint64_t>(blockIdx.x) * a.n;
+  const WarpScratch w = warp_scratch(a);
+  i128 acc = 0;
+  ull units = 0;
+  for (;;) {
+    const ull v1 = next_center(a, &center_sh);
+    if (v1 >= a.n) break;
+    const ull o1 = a.off[v1];
+    const uint32_t d1 = static_cast<uint32_t>(a.off[v1 + 1] - o1);
+    if (d1 == 0 || !owns_center(a, v1)) continue;
+    dense_scatter(a, cnt, o1, d1, false);
+    __syncthreads();
+    for (uint32_t bb = wib; bb < d1; bb += nw) {
+      if (lane == 0) ++units;
+      const uint32_t v0 = a.adj[o1 + bb];
+      const ull e = a.t.rev[o1 + bb];
+      const ull oo = a.off[v0];
+      const uint32_t d0 = static_cast<uint32_t>(a.off[v0 + 1] - oo);
+      const uint32_t p1 = static_cast<uint32_t>(e - oo);
+      const uint32_t* P = a.t.tent + a.t.toff[e];
+      const uint32_t np = a.t.tri[e];
+      if (np == 0) continue;
+      const uint32_t i0 = lb32(a.adj + oo, d0, v0);
+      if (lane == 0) nt_sh[wib] = 0;
+      for (uint32_t j = lane; j < np; j += 32) atomicOr(&w.bm[P[j] >> 5], 1u << (P[j] & 31));
+      __syncwarp();
+      ull T1 = 0;
+      flat_entries(
+          a, oo, P, np,
+          [&](uint32_t j, ull f2, uint32_t t02, ull to2) -> uint32_t {
+            if (P[j] >= i0) return 0u;  // v2 < v0 only
+            const ull C = a.t.k4[to2 + lb32(a.t.tent + to2, t02, p1)];  // |T(v0,v2) & P|
+            const uint32_t tri12 = a.t.tri[o1 + lb32(a.adj + o1, d1, a.adj[f2])];
+            T1 += (t02 - C - 1) * (static_cast<ull>(d1) - np - tri12 + C);
+            return 1u;
+          },
+          [&](int, uint32_t, uint32_t x, ull, uint32_t bounded) {
+            if (!bit(w.bm, x) && x != p1) {
+              if (atomicAdd(&w.t0[x], 1u) == 0u) w.touched[atomicAdd(&nt_sh[wib], 1u)] = x;
+              if (bounded) atomicAdd(&w.t1[x], 1u);
+            }
+          },
+          [](uint32_t, int) {});
+      T1 = warp_sum(T1);
+      __syncwarp();
+      const uint32_t nt = nt_sh[wib];
+      ull T2 = 0, T3 = 0;
+      for (uint32_t z = lane; z < nt; z += 32) {
+        const uint32_t x = w.touched[z];
+        w.touched[z] = 0u;
+        const ull A = w.t0[x], B = w.t1[x];
+        w.t0[x] = 0u;
+        w.t1[x] = 0u;
+        T2 += B * cnt[a.adj[oo + x]];
+        T3 += B * A;
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < np; j += 32) w.bm[P[j] >> 5] = 0u;
+      T2 = warp_sum(T2);
+      T3 = warp_sum(T3);
+      __syncwarp();
+      if (lane == 0) acc += static_cast<i128>(T1) - static_cast<i128>(T2) + static_cast<i128>(T3);  // T1 summed above
+    }
+    __syncthreads();
+    dense_scatter(a, cnt, o1, d1, true);
+  }
+  store_partial(a, acc, units);
+}
+
+// Ego-network pass, full mode, one warp per slot (t, a) of this shard:
+//   house: sum_{x not in N_L[a]} cl(x) (cl(x) - 1)
+//   tdb:   sum_{x not in N_L[a]} cl(x) cl2(x), cl2 from y in N_L(a) with y > t
+template <int KIND>
+__global__ void __launch_bounds__(kFastThreads) ego_full_kernel(const FastArgs a) {
+  __shared__ uint32_t nt_sh[kFastThreads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const WarpScratch w = warp_scratch(a);
+  i128 acc = 0;
+  uint64_t e0;
+  while (grab_chunk(a, lane, e0)) {
+    const uint64_t me = e0 + lane;
+    unsigned todo = __ballot_sync(kAll, me < a.e_hi && a.t.tri[me < a.e_hi ? me : 0] > 0);
+    while (todo) {
+      const int jl = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const ull e = e0 + jl;
+      const uint32_t t = a.src[e];
+      const ull to = a.off[t];
+      const uint32_t pa = static_cast<uint32_t>(e - to);
+      const uint32_t* Ta = a.t.tent + a.t.toff[e];
+      const uint32_t na = a.t.tri[e];
+      const uint32_t it = KIND == kFastTailedDiamondB
+                              ? lb32(a.adj + to, static_cast<uint32_t>(a.off[t + 1] - to), t) : 0u;
+      if (lane == 0) nt_sh[wib] = 0;
+      for (uint32_t j = lane; j < na; j += 32) atomicOr(&w.bm[Ta[j] >> 5], 1u << (Ta[j] & 31));
+      __syncwarp();
+      flat_entries(
+          a, to, Ta, na,
+          [&](uint32_t j, ull, uint32_t, ull) -> uint32_t {
+            return (KIND == kFastTailedDiamondB && Ta[j] >= it) ? 1u : 0u;  // y > t
+          },
+          [&](int, uint32_t, uint32_t x, ull, uint32_t up) {
+            if (atomicAdd(&w.t0[x], 1u) == 0u) w.touched[atomicAdd(&nt_sh[wib], 1u)] = x;
+            if (up) atomicAdd(&w.t1[x], 1u);
+          },
+          [](uint32_t, int) {});
+      __syncwarp();
+      const uint32_t nt = nt_sh[wib];
+      ull s = 0;
+      for (uint32_t z = lane; z < nt; z += 32) {
+        const uint32_t x = w.touched[z];
+        w.touched[z] = 0u;
+        const ull c = w.t0[x];
+        w.t0[x] = 0u;
+        ull c2 = 0;
+        if (KIND == kFastTailedDiamondB) {
+          c2 = w.t1[x];
+          w.t1[x] = 0u;
+        }
+        if (!bit(w.bm, x) && x != pa) s += KIND == kFastHouse ? c * (c - 1) : c * c2;
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < na; j += 32) w.bm[Ta[j] >> 5] = 0u;
+      acc += static_cast<i128>(s);
+      __syncwarp();
+    }
+  }
+  store_partial(a, acc, 0);
+}
+
+// Tailed diamond (a), full mode: the per-unit terms except S6, one warp per
+// unit, the (v2, x) pairs flattened over the lanes (flat_entries).
+__global__ void __launch_bounds__(kFastThreads) tda_full_kernel(const FastArgs a) {
+  __shared__ uint32_t ntouched[kFastThreads / 32];
+  __shared__ uint32_t cnt_a[kFastThreads / 32][32], cnt_c[kFastThreads / 32][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const WarpScratch w = warp_scratch(a);
+  cnt_a[wib][lane] = 0;
+  cnt_c[wib][lane] = 0;
+  ull cnt = 0, units = 0;
+  bool ovf = false;
+  uint64_t e0;
+  while (grab_chunk(a, lane, e0)) {
+    bool mine;
+    const uint64_t e = unit_slot(a, e0 + lane, mine);
+    units += __popc(__ballot_sync(kAll, mine));
+    unsigned todo = __ballot_sync(kAll, mine && a.t.tri[mine ? e : 0] > 0);
+    while (todo) {
+      const int jl = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint64_t ue = __shfl_sync(kAll, static_cast<ull>(e), jl);
+      const uint32_t c = a.src[ue];
+      const ull c0 = a.off[c];
+      const uint32_t d1 = static_cast<uint32_t>(a.off[c + 1] - c0);
+      const uint32_t i0 = static_cast<uint32_t>(ue - c0);
+      const uint32_t* P = a.t.tent + a.t.toff[ue];
+      const uint32_t np = a.t.tri[ue];
+      if (lane == 0) ntouched[wib] = 0;
+      for (uint32_t j = lane; j < np; j += 32) atomicOr(&w.bm[P[j] >> 5], 1u << (P[j] & 31));
+      __syncwarp();
+      ull S2 = 0, S5 = 0;
+      flat_entries(
+          a, c0, P, np,
+          [&](uint32_t, ull, uint32_t t2, ull to2) -> uint32_t { return lb32(a.t.tent + to2, t2, i0); },
+          [&](int k, uint32_t r, uint32_t x, ull eidx, uint32_t lb) {
+            if (bit(w.bm, x)) {
+              atomicAdd(&cnt_c[wib][k], 1u);
+            } else if (r < lb) {
+              atomicAdd(&cnt_a[wib][k], 1u);
+              if (atomicAdd(&w.t0[x], 1u) == 0u) w.touched[atomicAdd(&ntouched[wib], 1u)] = x;
+              S5 += a.t.k4[eidx];
+            }
+          },
+          [&](uint32_t j, int k) {
+            const uint32_t t2 = a.t.tri[c0 + P[j]];
+            S2 += static_cast<ull>(cnt_a[wib][k]) * (t2 - cnt_c[wib][k]);
+            cnt_a[wib][k] = 0;
+            cnt_c[wib][k] = 0;
+          });
+      __syncwarp();
+      const uint32_t nt = ntouched[wib];
+      ull pairs = 0, S3 = 0, S4 = 0;
+      for (uint32_t z = lane; z < nt; z += 32) {
+        const uint32_t x = w.touched[z];
+        w.touched[z] = 0u;
+        const ull al = w.t0[x];
+        w.t0[x] = 0u;
+        pairs += al;
+        S3 += static_cast<ull>(a.t.tri[c0 + x]) * al;
+        S4 += al * al;
+      }
+      for (uint32_t j = lane; j < np; j += 32) w.bm[P[j] >> 5] = 0u;
+      pairs = warp_sum(pairs);
+      S2 = warp_sum(S2);
+      S3 = warp_sum(S3);
+      S4 = warp_sum(S4);
+      S5 = warp_sum(S5);
+      __syncwarp();
+      if (lane == jl) checked_add(cnt, static_cast<ull>(d1 - np) * pairs - S2 - S3 + S4 + S5, ovf);  // + S6 >= 0
+    }
+  }
+  flush(a, cnt, units, ovf, lane);
+}
+
+__global__ void k4_pairs_kernel(const uint32_t* __restrict__ k4, uint64_t entries, ull* out) {
+  ull s = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < entries;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const ull k = k4[i];
+    s += k * (k - (k ? 1 : 0));
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
 int cuda_fail(cudaError_t e, const char* what, std::string* err) {
@@ -1116,7 +1546,7 @@ int fast_kind(const smg_plan& p) {
 }
 
 uint64_t fast_scratch_words(int kind, uint64_t dmax) {
-  if (kind == kFastTailedDiamondA) return 2 * dmax + (dmax + 31) / 32 + 32;
+  if (kind == kFastTailedDiamondA) return 3 * dmax + (dmax + 31) / 32 + 32;  // WarpScratch layout
   if (kind == kFastHouse || kind == kFastTailedDiamondB || kind == kFastPath4) return 3 * dmax + (dmax + 31) / 32 + 32;
   if (kind == kFastRectangle || kind == kFastRectangleMotif) return (dmax + 31) / 32 + 32;  // per CTA (see fast_launch)
   return 0;
@@ -1124,7 +1554,7 @@ uint64_t fast_scratch_words(int kind, uint64_t dmax) {
 
 int fast_slot_arrays(int kind) {
   if (kind == kFastHouse) return 3;
-  if (kind == kFastPath4) return 1;
+  if (kind == kFastPath4 || kind == kFastRectangle || kind == kFastRectangleMotif) return 1;
   if (kind == kFastTailedDiamondB) return 2;
   return 0;
 }
@@ -1134,27 +1564,88 @@ bool fast_dense(int kind) {
          kind == kFastRectangleMotif;
 }
 
-int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st) {
+bool fast_has_full(int kind) {
+  return kind == kFastHouse || kind == kFastTailedDiamondA || kind == kFastTailedDiamondB;
+}
+
+int fast_launch_full(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st) {
+  if (kind == kFastTailedDiamondA) {  // per-unit terms without S6, checked sum into count
+    tda_full_kernel<<<blocks, kFastThreads, 0, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+  }
+  if (kind != kFastHouse && kind != kFastTailedDiamondB) return 2;
+  // centre pass -> part[0 .. blocks), ego pass -> part[blocks .. 2 blocks)
+  if (cudaMemsetAsync(a.part, 0, 4 * blocks * sizeof(ull), st) != cudaSuccess) return 1;
+  if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
+  if (kind == kFastHouse) house_full_center_kernel<<<blocks, kFastThreads, 0, st>>>(a);
+  else tdb_full_center_kernel<<<blocks, kFastThreads, 0, st>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  FastArgs w = a;
+  w.part = a.part + 2 * blocks;
+  if (kind == kFastHouse) ego_full_kernel<kFastHouse><<<blocks, kFastThreads, 0, st>>>(w);
+  else ego_full_kernel<kFastTailedDiamondB><<<blocks, kFastThreads, 0, st>>>(w);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int tindex_k4_pairs(const TIndex& t, int num_sms, cudaStream_t st, unsigned long long* out, std::string* err) {
+  ull* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(ull));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d, 0, sizeof(ull), st);
+  if (e == cudaSuccess && t.entries) {
+    k4_pairs_kernel<<<num_sms * 8, 256, 0, st>>>(t.k4, t.entries, d);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, sizeof(ull), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  return e == cudaSuccess ? 0 : cuda_fail(e, "k4 pairs", err);
+}
+
+bool fast_center_v1(int kind) {
+  return kind == kFastStar4 || kind == kFastTailedDiamondA || kind == kFastTailedTriangle;
+}
+
+int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st, bool combine_only) {
   if (kind == kFastStar4) {
     star4_kernel<<<blocks, kFastThreads, 0, st>>>(a);
   } else if (kind == kFastTailedDiamondA) {
-    tda_kernel<<<blocks, kFastThreads, 0, st>>>(a);
+    tda_kernel<false><<<blocks, kFastThreads, 0, st>>>(a);
   } else if (kind == kFastTailedTriangle) {
     star_kernel<kFastTailedTriangle><<<blocks, kFastThreads, 0, st>>>(a);
   } else if (kind == kFastDiamond) {
     star_kernel<kFastDiamond><<<blocks, kFastThreads, 0, st>>>(a);
   } else if (kind == kFastRectangle || kind == kFastRectangleMotif) {
-    if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
-    if (kind == kFastRectangle) rect_kernel<true><<<blocks, kFastThreads, 0, st>>>(a);
-    else rect_kernel<false><<<blocks, kFastThreads, 0, st>>>(a);
+    const bool array = a.acc0 != nullptr;  // root-range call: per-unit values, cached, then combined
+    if (!(array && combine_only)) {
+      if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
+      if (kind == kFastRectangle) {
+        if (array) rect_kernel<true, true><<<blocks, kFastThreads, 0, st>>>(a);
+        else rect_kernel<true, false><<<blocks, kFastThreads, 0, st>>>(a);
+      } else {
+        if (array) rect_kernel<false, true><<<blocks, kFastThreads, 0, st>>>(a);
+        else rect_kernel<false, false><<<blocks, kFastThreads, 0, st>>>(a);
+      }
+      if (cudaGetLastError() != cudaSuccess) return 1;
+    }
+    if (array) {
+      if (kind == kFastRectangle) combine_kernel<kFastRectangle><<<blocks, kFastThreads, 0, st>>>(a);
+      else combine_kernel<kFastRectangleMotif><<<blocks, kFastThreads, 0, st>>>(a);
+    }
   } else if (kind == kFastPath4) {
-    if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
-    house_eh_kernel<true><<<blocks, kFastThreads, 0, st>>>(a);
-    if (cudaGetLastError() != cudaSuccess) return 1;
+    if (!combine_only) {
+      if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
+      house_eh_kernel<true><<<blocks, kFastThreads, 0, st>>>(a);
+      if (cudaGetLastError() != cudaSuccess) return 1;
+    }
     combine_kernel<kFastPath4><<<blocks, kFastThreads, 0, st>>>(a);
   } else if (kind == kFastHouse || kind == kFastTailedDiamondB) {
     // (1) center-table pass, (2) ego-network pass, (3) combine; the queue
     // cursors are reset between passes on the stream
+    if (combine_only) {
+      if (kind == kFastHouse) combine_kernel<kFastHouse><<<blocks, kFastThreads, 0, st>>>(a);
+      else combine_kernel<kFastTailedDiamondB><<<blocks, kFastThreads, 0, st>>>(a);
+      return cudaGetLastError() == cudaSuccess ? 0 : 1;
+    }
     if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
     if (cudaMemsetAsync(a.acc2, 0, a.slots * sizeof(ull), st) != cudaSuccess) return 1;
     if (kind == kFastHouse) house_eh_kernel<false><<<blocks, kFastThreads, 0, st>>>(a);
@@ -1162,6 +1653,9 @@ int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st) {
     if (cudaGetLastError() != cudaSuccess) return 1;
     FastArgs w = a;  // the ego pass walks every slot (no shard map, no root filter)
     w.num_shards = 1;
+    w.e_lo = 0;
+    w.e_hi = a.slots;
+    w.via_rev = 0;
     w.next_chunk = a.next2;
     if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
     if (kind == kFastHouse) ego_w_kernel<kFastHouse><<<blocks, kFastThreads, 0, st>>>(w);

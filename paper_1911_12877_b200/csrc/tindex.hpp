@@ -48,6 +48,8 @@ struct FastArgs {
   const uint32_t* src;
   uint64_t n, slots;
   uint32_t root_lo, root_hi;           // units (v0, v1) with v0 in [root_lo, root_hi)
+  uint64_t e_lo, e_hi;                 // slots the unit kernels walk ([0, slots), or off[lo]..off[hi])
+  int via_rev;                         // the unit's own slot is the reverse of the walked one
   uint32_t num_shards;                 // > 1: shard map below
   const unsigned long long* map_begin;
   const unsigned long long* map_pref;
@@ -63,6 +65,9 @@ struct FastArgs {
   unsigned long long* acc2;            // slots
   uint32_t* dense;                     // blocks x n
   unsigned long long* next2;           // second queue cursor (zeroed by the caller)
+  // full-count mode (whole root range; house, tailed diamond a/b): signed
+  // partial sums, one 128-bit slot (lo, hi) per CTA, summed by the host
+  unsigned long long* part;            // blocks x 2
   unsigned long long* next_chunk;      // queue cursor (zeroed by the caller)
   unsigned long long* count;           // checked uint64 sum
   unsigned long long* units;
@@ -74,8 +79,19 @@ struct FastArgs {
 uint64_t fast_scratch_words(int kind, uint64_t dmax);
 int fast_slot_arrays(int kind);
 bool fast_dense(int kind);
-// Blocks x 256 threads, persistent.
-int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st);
+// Blocks x 256 threads, persistent.  combine_only: the per-slot accumulators
+// of this kind are still valid (a cached earlier full pass): only combine.
+int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st, bool combine_only);
+// Full-count mode: the per-unit sums of kind over this shard's units land in
+// a.part (signed); the host adds global terms (fast_global_terms).  Returns 0
+// when launched, 2 when the kind has no full mode.
+int fast_launch_full(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st);
+bool fast_has_full(int kind);
+// Sum over index entries of k4 * (k4 - 1) (every entry of the index; needs
+// the k4 array).  Synchronous.
+int tindex_k4_pairs(const TIndex& t, int num_sms, cudaStream_t st, unsigned long long* out, std::string* err);
+// Kinds whose units sit on the reverse slot (centre v1 = src of the unit slot).
+bool fast_center_v1(int kind);
 constexpr int kFastThreads = 256;
 
 }  // namespace smg

@@ -72,22 +72,25 @@ def shard_slots(offsets, adjacency, shard: int, num_shards: int, unit_bound: boo
 
 
 def split_u64(values):
+    """Exact integers (a shard's share may be signed and exceed 64 bits) as
+    three int64 lanes: bits 0-31, bits 32-63, and the signed rest."""
     lo = [int(v) & 0xFFFFFFFF for v in values]
-    hi = [int(v) >> 32 for v in values]
-    return lo + hi
+    mid = [(int(v) >> 32) & 0xFFFFFFFF for v in values]
+    hi = [int(v) >> 64 for v in values]
+    return lo + mid + hi
 
 
-def join_u64(halves, k, check_overflow=(0,)):
-    lo, hi = halves[:k], halves[k:]
-    out = [int(h) * (1 << 32) + int(l) for l, h in zip(lo, hi)]
+def join_u64(lanes, k, check_overflow=(0,)):
+    lo, mid, hi = lanes[:k], lanes[k:2 * k], lanes[2 * k:3 * k]
+    out = [int(h) * (1 << 64) + int(m) * (1 << 32) + int(l) for l, m, h in zip(lo, mid, hi)]
     for i in check_overflow:
-        if out[i] >= 1 << 64:
+        if not 0 <= out[i] < 1 << 64:
             raise N.CountOverflowError("embedding count exceeds 64 bits")
     return out
 
 
 def allreduce_u64(values, group=None, device=None):
-    """Exact elementwise sum of uint64 values over the process group."""
+    """Exact elementwise sum of integers over the process group."""
     import torch
     import torch.distributed as dist
     k = len(values)
@@ -98,7 +101,7 @@ def allreduce_u64(values, group=None, device=None):
 
 def checked_total(values) -> int:
     total = sum(int(v) for v in values)
-    if total >= 1 << 64:
+    if not 0 <= total < 1 << 64:
         raise N.CountOverflowError("embedding count exceeds 64 bits")
     return total
 
@@ -109,6 +112,6 @@ def count_distributed(graph, plan, rank: int, world: int, device: int = 0, meter
     shard_fn = shard_fn or count_shard
     r = shard_fn(graph, plan, rank, world, device=device, meter=meter)
     tot = allreduce_u64([r.count, r.elements, r.units], group=group, device=comm_device)
-    if tot[0] >= 1 << 64:
+    if not 0 <= tot[0] < 1 << 64:
         raise N.CountOverflowError("embedding count exceeds 64 bits")
     return CountResult(tot[0], [r.count], tot[1], tot[2], r.wall_ms, r.kernel_ms)

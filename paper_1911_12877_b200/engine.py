@@ -34,7 +34,9 @@ class CountResult:
 
 
 def _result(r: N.SmgResult, ngpu: int) -> CountResult:
-    return CountResult(int(r.count), [int(r.per_gpu[i]) for i in range(ngpu)], int(r.elements),
+    # count_hi: a shard's share of a folded full count may be signed (128-bit)
+    count = (int(r.count_hi) << 64) + int(r.count)
+    return CountResult(count, [int(r.per_gpu[i]) for i in range(ngpu)], int(r.elements),
                        int(r.units), float(r.wall_ms), float(r.kernel_ms))
 
 
@@ -46,8 +48,9 @@ def _plan(plan) -> Plan:
     raise N.InputError("plan must be a Plan or plan JSON")
 
 
-def _flags(meter: bool, generic: bool) -> int:
-    return (N.SMG_METER if meter else 0) | (N.SMG_GENERIC if generic else 0)
+def _flags(meter: bool, generic: bool, folded: bool = False) -> int:
+    return (N.SMG_METER if meter else 0) | (N.SMG_GENERIC if generic else 0) | \
+        (N.SMG_FOLDED_RANGE if folded else 0)
 
 
 def count_result(graph: Graph, plan, gpus: int = 1, meter: bool = False, generic: bool = False) -> CountResult:
@@ -80,13 +83,15 @@ def motif_counts(graph: Graph, k: int, gpus: int = 1) -> list[dict]:
 
 
 def count_range(graph: Graph, plan, lo: int, hi: int, device: int = 0, meter: bool = False,
-                generic: bool = False) -> CountResult:
+                generic: bool = False, folded: bool = False) -> CountResult:
+    """Executor::count_range(lo, hi).  folded=True: the folded per-unit passes
+    even for the two-centre kinds (default: the generic executor there)."""
     p = _plan(plan)
     lib = N.gpu_lib()
     h = graph.device_handle((device,))
     sp = p.to_smg()
     r = N.SmgResult()
-    N.check_gpu(lib.smg_count_range(h, ctypes.byref(sp), 0, lo, hi, _flags(meter, generic),
+    N.check_gpu(lib.smg_count_range(h, ctypes.byref(sp), 0, lo, hi, _flags(meter, generic, folded),
                                     ctypes.byref(r)))
     return _result(r, 1)
 

@@ -55,11 +55,17 @@ def test_folded_kinds_are_recognised():
 def test_folded_per_root_vs_reference(reference, n, p, seed):
     g = Graph.from_edges(*er_graph(n, p, seed))
     rg = reference.graph_from_csr(g.offsets, g.adjacency)
+    bad = []
     for name, plan in folded_plans().items():
         want, _ = rg.count_roots(plan.to_json(), np.arange(g.n, dtype=np.uint32), 4)
-        got = [count_range(g, plan, v, v + 1).count for v in range(g.n)]
-        assert got == [int(x) for x in want], name
-        assert count_result(g, plan).count == int(want.sum())
+        want = [int(x) for x in want]
+        got = [count_range(g, plan, v, v + 1, folded=True).count for v in range(g.n)]
+        gen = [count_range(g, plan, v, v + 1, generic=True).count for v in range(g.n)]
+        full = count_result(g, plan).count
+        if got != want or full != sum(want):
+            diff = [(v, got[v], want[v], gen[v]) for v in range(g.n) if got[v] != want[v]][:4]
+            bad.append((name, full, sum(want), sum(got), sum(gen), diff))
+    assert not bad, bad
 
 
 @pytest.mark.gpu
@@ -71,15 +77,20 @@ def test_folded_per_root_vs_reference(reference, n, p, seed):
                          ids=lambda s: s.tag)
 def test_folded_vs_generic_and_oracle(spec, port):
     g = configs.load(spec)
+    bad = []
     for name, plan in folded_plans().items():
         fast = count_result(g, plan)
         gen = count_result(g, plan, generic=True)
-        assert fast.count == gen.count, name
-        assert fast.units == gen.units, name
+        if fast.count != gen.count or fast.units != gen.units:
+            bad.append((name, fast.count, gen.count, fast.units, gen.units))
+            continue
         if g.n <= 6000:
             c, _ = port.count(g.offsets, g.adjacency, plan.to_smg(), threads=8)
             assert fast.count == c, name
         parts = [count_shard(g, plan, i, 3) for i in range(3)]
         assert sum(r.count for r in parts) == fast.count
         lo, hi = g.n // 3, g.n // 2
-        assert count_range(g, plan, lo, hi).count == count_range(g, plan, lo, hi, generic=True).count
+        want = count_range(g, plan, lo, hi, generic=True).count
+        assert count_range(g, plan, lo, hi).count == want, name
+        assert count_range(g, plan, lo, hi, folded=True).count == want, name
+    assert not bad, bad

@@ -30,7 +30,7 @@ def test_engine_library_exports_every_declared_symbol():
     assert "smg_count" in names and "smg_graph_create" in names
     for name in names:
         assert hasattr(lib, name), name
-    assert lib.smg_abi_version() == 1
+    assert lib.smg_abi_version() == 2  # smg_result gained count_hi
 
 
 def test_graph_library_exports_every_declared_symbol():
