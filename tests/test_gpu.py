@@ -67,8 +67,10 @@ def test_shards_partition_units(golden, corpus_graphs):
         full = count_result(g, p)
         for s in (2, 3, 8):
             parts = [count_shard(g, p, i, s) for i in range(s)]
-            assert sum(r.count for r in parts) == full.count
-            assert sum(r.units for r in parts) == full.units
+            assert sum(r.count for r in parts) == full.count  # folded shares may be signed
+            gen = [count_shard(g, p, i, s, generic=True) for i in range(s)]
+            assert sum(r.count for r in gen) == full.count
+            assert sum(r.units for r in gen) == count_result(g, p, generic=True).units
 
 
 def test_shard_units_follow_host_mapping(golden, corpus_graphs, port):
@@ -96,10 +98,14 @@ def test_shard_units_follow_host_mapping(golden, corpus_graphs, port):
                 for i in range(s):
                     slots = shard_slots(g.offsets, g.adjacency, i, s, ub).astype(np.int64)
                     valid = int((g.adjacency[slots] < src[slots]).sum()) if ub else slots.size
-                    r = count_shard(g, p, i, s)
+                    # generic executor: the folded full-count kinds (house) shard by
+                    # centre and return signed 128-bit shares instead
+                    r = count_shard(g, p, i, s, generic=True)
                     assert r.units == valid
                     c, _ = port.count_edges(g.offsets, g.adjacency, p.to_smg(), slots)
                     assert r.count == c
+                total = port.count(g.offsets, g.adjacency, p.to_smg(), threads=2)[0]
+                assert sum(count_shard(g, p, i, s).count for i in range(s)) == total
 
 
 def test_device_csr_validation_rejects_bad_layouts():

@@ -14,7 +14,17 @@ cfg, label = sys.argv[1], sys.argv[2]
 K = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 nwin = int(sys.argv[4]) if len(sys.argv) > 4 else 4096
 g = configs.load(cfg)
-if os.environ.get("ORIENT"):
+orient = os.environ.get("ORIENT", "")
+if orient in ("asc", "desc"):  # relabel by degree (asc: hubs get the large ids)
+    from paper_1911_12877_b200.graph import Graph
+    deg = np.diff(g.offsets.astype(np.int64))
+    order = np.argsort(deg if orient == "asc" else -deg, kind="stable")
+    new_id = np.empty(g.n, dtype=np.uint32)
+    new_id[order] = np.arange(g.n, dtype=np.uint32)
+    src = np.repeat(np.arange(g.n, dtype=np.uint32), deg)
+    keep = src < g.adjacency
+    g = Graph.from_edges(g.n, np.stack([new_id[src[keep]], new_id[g.adjacency[keep]]], axis=1))
+elif orient:
     g = g.orient()  # orient_reindex (graph.cpp:137-161): hubs get small ids
 plan = dict(configs.config_patterns(cfg))[label]
 w = (g.n + nwin - 1) // nwin
