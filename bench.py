@@ -289,11 +289,12 @@ def load_profile(cfg, label):
 
 # kernels one full count launches: the generic executor runs count_kernel (+
 # heavy_kernel for batched leaves); the folded kinds (tindex.cu, FastKind) run
-# one kernel (star4, tailed diamond a, tailed triangle, diamond, both rectangle
-# plans), or a centre-table pass and an ego-network pass (house, tailed diamond
-# b in full-count mode), or a centre pass and a combine (path4).  The triangle
+# one kernel (star4, tailed diamond a, tailed triangle, diamond), or a
+# centre-table pass and an ego-network pass (house, tailed diamond b in
+# full-count mode), or a centre pass and a combine (path4); the rectangle plans
+# run the 4-clique count_kernel, c4_kernel and tri_pairs_kernel.  The triangle
 # index, K5 and the k4 pair sum are built once per graph (cached).
-FOLDED_LAUNCHES = {1: 1, 2: 1, 3: 2, 4: 2, 5: 1, 6: 1, 7: 2, 8: 1, 9: 1}
+FOLDED_LAUNCHES = {1: 1, 2: 1, 3: 2, 4: 2, 5: 1, 6: 1, 7: 2, 8: 3, 9: 3}
 # configs whose E (intersected elements) the generic executor's
 # metering pass measures in seconds; the others report count time only
 METERED_CONFIGS = ("cfg1", "cfg2")

@@ -43,21 +43,36 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def _engine_sources() -> list[str]:
-    return (sorted(glob.glob(os.path.join(CSRC, "*.cu"))) +
-            sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) +
-            [os.path.join(CSRC, "program.hpp"), os.path.join(INCLUDE, "symmine_gpu.h")])
+def _engine_headers() -> list[str]:
+    return (sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(CSRC, "*.hpp"))) +
+            sorted(glob.glob(os.path.join(INCLUDE, "*.h"))))
 
 
 def build_engine(force: bool = False, verbose: bool = False) -> str:
-    srcs = _engine_sources()
-    if force or _stale(ENGINE_SO, srcs):
-        cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    """Each .cu is compiled to an object of its own (in parallel, only when it or
+    a header changed), then linked into libsymmine_gpu.so."""
+    from concurrent.futures import ThreadPoolExecutor
+    cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    hdr = _engine_headers()
+    objdir = os.path.join(CSRC, "_obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    jobs = []
+    for src in cu:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if force or _stale(obj, [src, *hdr]):
+            cmd = [_nvcc(), *flags, "-I", INCLUDE, "-c", "-o", obj, src]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            jobs.append(cmd)
+    if jobs:
+        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+            list(ex.map(lambda c: subprocess.run(c, check=True), jobs))
+    objs = [os.path.join(objdir, os.path.basename(src)[:-3] + ".o") for src in cu]
+    if force or jobs or _stale(ENGINE_SO, objs):
         tmp = ENGINE_SO + ".tmp"
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp, *cu]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+        subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs],
+                       check=True)
         os.replace(tmp, ENGINE_SO)
     return ENGINE_SO
 

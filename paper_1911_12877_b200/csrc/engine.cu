@@ -2324,6 +2324,12 @@ struct Replica {
   __int128 post_global = 0;
   uint32_t* fast_dense = nullptr;                      // per-CTA dense codegree tables
   size_t fast_dense_bytes = 0;
+  // degree-ordered copy of the CSR (orient_reindex ids: 0 = highest degree),
+  // built on first use for the label-free full counts (cliques, 4-cycles)
+  DevCSR ocsr;
+  bool view_oriented = false;                          // off/adj/src currently point at ocsr
+  bool map_oriented = false;                           // labelling the cached shard map belongs to
+  double post_extra_ms = 0;                            // device time of sub-counts finish() adds
   std::mutex mu;
 };
 
@@ -2437,7 +2443,11 @@ struct Launch {
 // a level-1 bound, built on r's device and cached on the replica (the graph is
 // immutable).  Caller holds r.mu.
 int ensure_shard_map(const smg_graph& g, Replica& r, uint32_t num_shards, int unit_bound) {
-  if (r.map_shards == num_shards && r.map_unit_bound == unit_bound && r.map_dev) return SMG_OK;
+  if (r.map_shards == num_shards && r.map_unit_bound == unit_bound && r.map_dev &&
+      r.map_oriented == r.view_oriented)
+    return SMG_OK;
+  r.map_shards = 0;  // invalid until rebuilt for this labelling
+  r.map_oriented = r.view_oriented;
   const uint64_t nch = (g.slots + kChunk - 1) / kChunk;
   const uint32_t J = num_shards * kShardSplit;
   cudaStream_t st = r.active();
@@ -2808,6 +2818,184 @@ int enqueue_fast(const smg_graph& g, Replica& r, int kind, const smg_plan& plan,
   return SMG_OK;
 }
 
+// ---- label-free full counts on the degree-ordered copy of the CSR ---------
+// A plan whose restrictions leave exactly one (or a fixed number) of the
+// automorphic embeddings of every instance counts the same total under any
+// relabelling of the vertices.  That holds for every clique plan (the
+// automorphism group is the full symmetric group, so the number of orderings
+// of an instance that satisfy a given set of id constraints does not depend
+// on the ids) and for the two rectangle plans fast_kind() recognises.  Their
+// full counts run on the orient_reindex copy (graph.cpp:137-161: ids by
+// descending degree), where every vertex has few smaller-id neighbours, so the
+// v_a < v_b cut-offs prune hub lists first.  Root-range calls, metering and
+// SMG_GENERIC calls keep the caller's labelling (per-root counts and E are
+// label-dependent).  SMG_RELABEL=0 turns it off.
+const int g_relabel = [] {
+  const char* e = std::getenv("SMG_RELABEL");
+  return (e && *e == '0') ? 0 : 1;
+}();
+
+bool clique_plan(const smg_plan& p) {
+  if (p.depth < 3) return false;
+  for (uint32_t i = 1; i < p.depth; ++i)
+    if (p.isect_mask[i] != static_cast<uint8_t>((1u << i) - 1u) || p.diff_mask[i]) return false;
+  return true;
+}
+
+int ensure_oriented(const smg_graph& g, Replica& r) {
+  if (r.ocsr.off) return SMG_OK;
+  SMG_CUDA(cudaSetDevice(r.device));
+  DevCSR in;
+  in.off = r.off;
+  in.adj = r.adj;
+  in.src = r.src;
+  in.n = g.n;
+  in.slots = g.slots;
+  in.max_degree = g.max_degree;
+  std::string err;
+  const auto t0 = std::chrono::steady_clock::now();
+  DevCSR o;
+  if (device_orient(r.device, r.active(), r.num_sms, in, &o, nullptr, &err)) return fail(SMG_EIO, "orient: " + err);
+  r.ocsr = o;
+  if (g_trace)
+    std::fprintf(stderr, "[smg trace] degree-ordered CSR ready in %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  return SMG_OK;
+}
+
+// Points the replica's CSR at the degree-ordered copy for its lifetime.
+struct OrientedView {
+  Replica& r;
+  unsigned long long* off;
+  uint32_t* adj;
+  uint32_t* src;
+  explicit OrientedView(Replica& rep) : r(rep), off(rep.off), adj(rep.adj), src(rep.src) {
+    r.off = r.ocsr.off;
+    r.adj = r.ocsr.adj;
+    r.src = r.ocsr.src;
+    r.view_oriented = true;
+  }
+  ~OrientedView() {
+    r.off = off;
+    r.adj = adj;
+    r.src = src;
+    r.view_oriented = false;
+  }
+  OrientedView(const OrientedView&) = delete;
+  OrientedView& operator=(const OrientedView&) = delete;
+};
+
+// 1: clique plan (generic executor on the oriented view); 2: rectangle kinds
+// (c4_launch); 0: keep the caller's labelling.
+int relabel_mode(const smg_plan& plan, uint32_t flags) {
+  if (!g_relabel || (flags & (SMG_METER | SMG_GENERIC))) return 0;
+  if (clique_plan(plan)) return 1;
+  if (!g_fast) return 0;
+  const int k = fast_kind(plan);
+  return (k == kFastRectangle || k == kFastRectangleMotif) ? 2 : 0;
+}
+
+int enqueue_oriented(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
+  int rc = ensure_oriented(g, r);
+  if (rc) return rc;
+  OrientedView view(r);
+  return enqueue(g, r, prog, L);
+}
+
+// Induced 4-cycles of the whole graph (both rectangle plans), this shard's
+// share: C4 - D over the shard's centres / slot chunks (c4_launch) + 3 x the
+// shard's share of the 4-clique count.
+int enqueue_c4(const smg_graph& g, Replica& r, int kind, const Launch& L) {
+  r.post_kind = 0;
+  r.post_extra_ms = 0;
+  int rc = ensure_oriented(g, r);
+  if (rc) return rc;
+  OrientedView view(r);
+  // K4 share: the clique plan v0 > v1 > v2 > v3 through the generic executor
+  unsigned long long k4 = 0;
+  double k4_ms = 0;
+  {
+    smg_plan p;
+    std::memset(&p, 0, sizeof(p));
+    p.depth = 4;
+    for (int i = 0; i < SMG_MAX_LEVELS; ++i) p.parent[i] = -1;
+    for (int i = 1; i < 4; ++i) {
+      p.isect_mask[i] = static_cast<uint8_t>((1u << i) - 1u);
+      p.parent[i] = static_cast<int8_t>(i - 1);
+    }
+    p.flags = SMG_PLAN_USE_BOUNDS | SMG_PLAN_USE_RESTRICTIONS;
+    Program prog;
+    const std::string err = compile_program(p, &prog);
+    if (!err.empty()) return fail(SMG_EIO, "internal clique plan: " + err);
+    Launch K = L;
+    K.meter = false;
+    K.meter_roots = false;
+    rc = enqueue(g, r, prog, K);
+    if (rc) return rc;
+    uint64_t c = 0, el = 0, u = 0;
+    bool ovf = false;
+    rc = finish(r, &c, &el, &u, &ovf, &k4_ms);
+    if (rc) return rc;
+    if (ovf) return fail(SMG_EOVERFLOW, "4-clique count exceeds 64 bits");
+    k4 = c;
+  }
+  cudaStream_t st = r.active();
+  const unsigned blocks = static_cast<unsigned>(r.num_sms) * 2;
+  const size_t dense_need = static_cast<size_t>(blocks) * std::max<uint64_t>(g.n, 1) * sizeof(uint32_t);
+  if (dense_need > r.fast_dense_bytes) {
+    if (r.fast_dense) cudaFree(r.fast_dense);
+    r.fast_dense = nullptr;
+    r.fast_dense_bytes = 0;
+    SMG_CUDA(cudaMalloc(&r.fast_dense, dense_need));
+    SMG_CUDA(cudaMemsetAsync(r.fast_dense, 0, dense_need, st));
+    r.fast_dense_bytes = dense_need;
+  }
+  const size_t words = 4 * static_cast<size_t>(blocks);
+  if (words > r.part_words) {
+    if (r.part_dev) cudaFree(r.part_dev);
+    if (r.part_host) cudaFreeHost(r.part_host);
+    r.part_dev = nullptr;
+    r.part_host = nullptr;
+    r.part_words = 0;
+    SMG_CUDA(cudaMalloc(&r.part_dev, words * sizeof(unsigned long long)));
+    SMG_CUDA(cudaMallocHost(&r.part_host, words * sizeof(unsigned long long)));
+    r.part_words = words;
+  }
+  FastArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.off = r.off;
+  a.adj = r.adj;
+  a.src = r.src;
+  a.n = g.n;
+  a.slots = g.slots;
+  a.root_hi = static_cast<uint32_t>(g.n);
+  a.e_hi = g.slots;
+  a.num_shards = L.num_shards;
+  a.shard = L.shard;
+  a.dmax = g.max_degree;
+  a.dense = r.fast_dense;
+  a.part = r.part_dev;
+  a.next_chunk = &r.ctr->next_chunk;
+  a.next2 = &r.ctr->heavy_next;
+  a.count = &r.ctr->count;
+  a.units = &r.ctr->units;
+  a.overflow = &r.ctr->overflow;
+  SMG_CUDA(cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st));
+  SMG_CUDA(cudaEventRecord(r.ev0, st));
+  if (g.slots && c4_launch(a, blocks, st)) return fail(SMG_EIO, "4-cycle kernel launch failed");
+  SMG_CUDA(cudaMemcpyAsync(r.part_host, r.part_dev, 4 * blocks * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+  SMG_CUDA(cudaGetLastError());
+  SMG_CUDA(cudaEventRecord(r.ev1, st));
+  SMG_CUDA(cudaMemcpyAsync(r.host_ctr, r.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  r.post_kind = kind;
+  r.post_blocks = blocks;
+  r.post_global = static_cast<__int128>(k4) * 3;
+  r.post_extra_ms = k4_ms;
+  if (!g.slots) std::memset(r.part_host, 0, 4 * blocks * sizeof(unsigned long long));
+  return SMG_OK;
+}
+
 // The folded kernel for this call, or kFastNone.  range: a root-range call.
 int fast_for(const smg_plan& plan, uint32_t flags, bool range = false) {
   if (!g_fast || (flags & (SMG_METER | SMG_GENERIC))) return kFastNone;
@@ -2845,7 +3033,8 @@ int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* 
   *elems = r.host_ctr->elements;
   *units = r.host_ctr->units;
   *ovf = r.host_ctr->overflow != 0;
-  *ms = t;
+  *ms = t + r.post_extra_ms;
+  r.post_extra_ms = 0;
   if (count_hi) *count_hi = 0;
   if (r.post_kind) {
     // centre partials [0, B), ego partials [B, 2B) as (lo, hi) pairs
@@ -2966,6 +3155,9 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->fast_scratch) cudaFree(r->fast_scratch);
     if (r->fast_acc) cudaFree(r->fast_acc);
     if (r->fast_dense) cudaFree(r->fast_dense);
+    if (r->ocsr.off) cudaFree(r->ocsr.off);
+    if (r->ocsr.adj) cudaFree(r->ocsr.adj);
+    if (r->ocsr.src) cudaFree(r->ocsr.src);
     if (r->part_dev) cudaFree(r->part_dev);
     if (r->part_host) cudaFreeHost(r->part_host);
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
@@ -3251,7 +3443,11 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
   L.num_shards = num_shards;
   {
     const int fk = fast_for(*plan, flags);
-    rc = fk ? enqueue_fast(*g, r, fk, *plan, L) : enqueue(*g, r, prog, L);
+    const int rm = relabel_mode(*plan, flags);
+    rc = rm == 2   ? enqueue_c4(*g, r, fk, L)
+         : rm == 1 ? enqueue_oriented(*g, r, prog, L)
+         : fk      ? enqueue_fast(*g, r, fk, *plan, L)
+                   : enqueue(*g, r, prog, L);
   }
   if (rc) return rc;
   bool ovf = false;
@@ -3433,7 +3629,12 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
     L.shard = d;
     L.num_shards = num_gpus;
     const int fk = fast_for(*plan, flags);
-    rc = fk ? enqueue_fast(*g, *g->reps[d], fk, *plan, L) : enqueue(*g, *g->reps[d], prog, L);
+    const int rm = relabel_mode(*plan, flags);
+    Replica& rd = *g->reps[d];
+    rc = rm == 2   ? enqueue_c4(*g, rd, fk, L)
+         : rm == 1 ? enqueue_oriented(*g, rd, prog, L)
+         : fk      ? enqueue_fast(*g, rd, fk, *plan, L)
+                   : enqueue(*g, rd, prog, L);
     if (rc) {
       // devices 0..d-1 are still counting into their Counters: drain them
       // before the replica locks are released

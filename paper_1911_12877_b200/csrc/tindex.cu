@@ -1564,6 +1564,129 @@ bool fast_dense(int kind) {
          kind == kFastRectangleMotif;
 }
 
+// ------------------------------------------- induced 4-cycles, full count ---
+// Both rectangle plans count every induced 4-cycle of the graph exactly once
+// (their restrictions leave one of the 8 automorphic embeddings), so the full
+// count does not depend on the vertex labels.  On the degree-ordered copy of
+// the CSR (orient_reindex: id 0 = highest degree; engine.cu keeps one per
+// replica) the count is assembled from three label-free sums:
+//     induced C4 = C4 - D + 3 K4
+//   C4 = sum_c sum_{x > c} C(w_c(x), 2), w_c(x) = #{u in N(c) & N(x) : u > c}:
+//        every 4-cycle (as a subgraph) at its smallest vertex c, opposite x;
+//        only wedges c - u - x with u, x > c are walked, sum_u d(u) d-(u)
+//        elements instead of sum_u d(u)^2 (d- = neighbours of higher degree);
+//   D  = sum_{edges e} C(tri(e), 2): diamonds (K4 minus an edge) as subgraphs,
+//        = induced diamonds + 6 K4;  C4 = induced C4 + induced diamonds + 3 K4;
+//   K4 = the 4-clique count (generic executor, clique-local path).
+// c4_kernel: one CTA per centre c, dense per-CTA table w_c (n words, kept
+// zero between centres).  Each touch adds atomicAdd's return value: the k-th
+// increment of a word returns k - 1, and 0 + 1 + ... + (w - 1) = C(w, 2).
+__global__ void __launch_bounds__(kFastThreads) c4_kernel(const FastArgs a) {
+  __shared__ ull center_sh;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t* cnt = a.dense + static_cast<uint64_t>(blockIdx.x) * a.n;
+  i128 acc = 0;
+  ull units = 0;
+  for (;;) {
+    const ull c = next_center(a, &center_sh);
+    if (c >= a.n) break;
+    if (a.num_shards > 1 && c % a.num_shards != a.shard) continue;
+    const ull co = a.off[c];
+    const uint32_t dc = static_cast<uint32_t>(a.off[c + 1] - co);
+    const uint32_t k0 = lb32(a.adj + co, dc, static_cast<uint32_t>(c) + 1u);  // first u > c
+    const uint32_t np = dc - k0;
+    if (threadIdx.x == 0) units += np;  // level-1 units (v1 < v0): one per undirected edge
+    if (np < 2) continue;
+    const uint32_t* U = a.adj + co + k0;
+    ull s = 0;
+    for (uint32_t j = wib; j < np; j += nw) {
+      const uint32_t u = U[j];
+      const ull uo = a.off[u];
+      const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
+      // x in N(u), x > c: c itself is in N(u), the suffix starts right after it
+      const uint32_t x0 = lb32(a.adj + uo, du, static_cast<uint32_t>(c) + 1u);
+      for (uint32_t k = x0 + lane; k < du; k += 32) s += atomicAdd(&cnt[a.adj[uo + k]], 1u);
+    }
+    acc += static_cast<i128>(s);
+    __syncthreads();
+    for (uint32_t j = wib; j < np; j += nw) {
+      const uint32_t u = U[j];
+      const ull uo = a.off[u];
+      const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
+      const uint32_t x0 = lb32(a.adj + uo, du, static_cast<uint32_t>(c) + 1u);
+      for (uint32_t k = x0 + lane; k < du; k += 32) cnt[a.adj[uo + k]] = 0u;
+    }
+  }
+  store_partial(a, acc, units);
+}
+
+// -D: minus sum over undirected edges (slot e = (u, v), u < v) of C(|N(u) & N(v)|, 2).
+__global__ void __launch_bounds__(kFastThreads) tri_pairs_kernel(const FastArgs a) {
+  const int lane = threadIdx.x & 31;
+  i128 acc = 0;
+  for (;;) {
+    ull chunk = 0;
+    if (lane == 0) chunk = atomicAdd(a.next_chunk, 1ull);
+    chunk = __shfl_sync(kAll, chunk, 0);
+    if (chunk * kSlotChunk >= a.slots) break;
+    if (a.num_shards > 1 && chunk % a.num_shards != a.shard) continue;
+    const uint64_t e = chunk * kSlotChunk + lane;
+    bool mine = e < a.slots;
+    uint32_t u = 0, v = 0;
+    if (mine) {
+      u = a.src[e];
+      v = a.adj[e];
+      mine = u < v;
+    }
+    ull bu = 0, bv = 0;
+    uint32_t du = 0, dv = 0;
+    if (mine) {
+      bu = a.off[u];
+      du = static_cast<uint32_t>(a.off[u + 1] - bu);
+      bv = a.off[v];
+      dv = static_cast<uint32_t>(a.off[v + 1] - bv);
+    }
+    const bool small = mine && min(du, dv) <= 8;
+    if (small) {
+      const ull t = isect_count(a.adj + bu, du, a.adj + bv, dv);
+      acc -= static_cast<i128>(t * (t - 1) / 2);
+    }
+    unsigned big = __ballot_sync(kAll, mine && !small);
+    while (big) {
+      const int j = __ffs(big) - 1;
+      big &= big - 1;
+      const ull jbu = __shfl_sync(kAll, bu, j), jbv = __shfl_sync(kAll, bv, j);
+      const uint32_t jdu = __shfl_sync(kAll, du, j), jdv = __shfl_sync(kAll, dv, j);
+      const bool su = jdu <= jdv;
+      const uint32_t* S = a.adj + (su ? jbu : jbv);
+      const uint32_t* L = a.adj + (su ? jbv : jbu);
+      const uint32_t ns = su ? jdu : jdv, nl = su ? jdv : jdu;
+      ull t = 0;
+      for (uint32_t i = lane; i < ns; i += 32) {
+        const uint32_t x = S[i];
+        const uint32_t p = lb32(L, nl, x);
+        t += (p < nl && L[p] == x) ? 1u : 0u;
+      }
+      t = warp_sum(t);
+      if (lane == 0) acc -= static_cast<i128>(t * (t - 1) / 2);
+    }
+  }
+  store_partial(a, acc, 0);
+}
+
+// C4 -> part[0 .. blocks), -D -> part[blocks .. 2 blocks) (a.off/adj/src: any
+// labelling of the graph, the degree-ordered one for speed).
+int c4_launch(const FastArgs& a, unsigned blocks, cudaStream_t st) {
+  if (cudaMemsetAsync(a.part, 0, 4 * blocks * sizeof(ull), st) != cudaSuccess) return 1;
+  if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
+  c4_kernel<<<blocks, kFastThreads, 0, st>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  FastArgs w = a;
+  w.part = a.part + 2 * blocks;
+  tri_pairs_kernel<<<blocks, kFastThreads, 0, st>>>(w);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 bool fast_has_full(int kind) {
   return kind == kFastHouse || kind == kFastTailedDiamondA || kind == kFastTailedDiamondB;
 }

@@ -51,6 +51,7 @@ struct FastArgs {
   uint64_t e_lo, e_hi;                 // slots the unit kernels walk ([0, slots), or off[lo]..off[hi])
   int via_rev;                         // the unit's own slot is the reverse of the walked one
   uint32_t num_shards;                 // > 1: shard map below
+  uint32_t shard;                      // this shard (c4_launch: centres / chunks dealt round-robin)
   const unsigned long long* map_begin;
   const unsigned long long* map_pref;
   uint32_t map_k;
@@ -87,6 +88,11 @@ int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st, b
 // when launched, 2 when the kind has no full mode.
 int fast_launch_full(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st);
 bool fast_has_full(int kind);
+// Induced 4-cycle full count, label-free form (see tindex.cu): C4 partials ->
+// a.part[0 .. 2 blocks), -D partials -> a.part[2 blocks .. 4 blocks); the
+// caller adds 3 K4.  Needs a.dense (blocks x n words, zero), a.next2,
+// a.next_chunk (zeroed), a.off/adj/src of the (degree-ordered) CSR.
+int c4_launch(const FastArgs& a, unsigned blocks, cudaStream_t st);
 // Sum over index entries of k4 * (k4 - 1) (every entry of the index; needs
 // the k4 array).  Synchronous.
 int tindex_k4_pairs(const TIndex& t, int num_sms, cudaStream_t st, unsigned long long* out, std::string* err);

@@ -94,3 +94,31 @@ def test_folded_vs_generic_and_oracle(spec, port):
         assert count_range(g, plan, lo, hi).count == want, name
         assert count_range(g, plan, lo, hi, folded=True).count == want, name
     assert not bad, bad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", [configs.GraphSpec("rmat", (12, 8, 0.57, 0.19, 0.19), 11),
+                                  configs.GraphSpec("chung_lu", (6000, 60000, 2.1, 600.0), 12),
+                                  configs.GraphSpec("er", (3000, 30000), 13)],
+                         ids=lambda s: s.tag)
+def test_label_free_full_counts(spec, port):
+    """Full counts of the clique plans (any restriction set) and the rectangle
+    plans run on the degree-ordered copy of the CSR (engine.cu, relabel_mode):
+    same totals and unit counts as the caller's labelling (generic=True keeps it)
+    and as the oracle, shard shares sum to the total, and a graph whose ids
+    are already degree-ordered (orient) gives the same totals."""
+    g = configs.load(spec)
+    go = g.orient()
+    plans = {f"clique:{k}": named_plan("clique", k) for k in (3, 4, 5)}
+    plans["clique:4 no restrictions"] = named_plan("clique", 4, use_restrictions=False)
+    plans["rectangle"] = named_plan("rectangle")
+    plans["rectangle_motif"] = {r["name"]: r["plan"] for r in motif_plans(4)}["rectangle"]
+    for name, plan in plans.items():
+        fast = count_result(g, plan)
+        gen = count_result(g, plan, generic=True)
+        c, _ = port.count(g.offsets, g.adjacency, plan.to_smg(), threads=8)
+        assert fast.count == gen.count == c, name
+        assert fast.units == gen.units, name
+        assert count_result(go, plan).count == c, name
+        for s in (2, 5):
+            assert sum(count_shard(g, plan, i, s).count for i in range(s)) == c, (name, s)

@@ -15,6 +15,7 @@ sys.path.insert(0, ROOT)
 ap = argparse.ArgumentParser()
 ap.add_argument("cfgs", nargs="*", default=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
 ap.add_argument("--cap", type=int, default=1800, help="per-pattern timeout (s)")
+ap.add_argument("--skip", nargs="*", default=[], help="pattern labels to leave out")
 ap.add_argument("--one", nargs=2, help=argparse.SUPPRESS)
 args = ap.parse_args()
 
@@ -41,6 +42,8 @@ os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 for cfg in args.cfgs:
     configs.load(cfg, verbose=True)
     for label, _ in configs.config_patterns(cfg):
+        if label in args.skip:
+            continue
         t = time.time()
         try:
             p = subprocess.run([sys.executable, __file__, "--one", cfg, label], capture_output=True, text=True,
