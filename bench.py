@@ -288,13 +288,13 @@ def load_profile(cfg, label):
 
 
 # kernels one full count launches: the generic executor runs count_kernel (+
-# heavy_kernel for batched leaves); the folded kinds (tindex.cu, FastKind) run
-# one kernel (star4, tailed diamond a, tailed triangle, diamond), or a
-# centre-table pass and an ego-network pass (house, tailed diamond b in
-# full-count mode), or a centre pass and a combine (path4); the rectangle plans
-# run the 4-clique count_kernel, c4_kernel and tri_pairs_kernel.  The triangle
+# heavy_kernel for batched leaves); tailed diamond a runs one folded kernel
+# (tindex.cu); house and tailed diamond b a centre-table pass and an
+# ego-network pass; the 4-vertex kinds (star4 1, tailed triangle 5, diamond 6,
+# path4 7, rectangle 8/9) the 4-clique count_kernel + m4_edge_kernel
+# (+ m4_vertex_kernel for 1, 5, 7; + c4_kernel for 7, 8, 9).  The triangle
 # index, K5 and the k4 pair sum are built once per graph (cached).
-FOLDED_LAUNCHES = {1: 1, 2: 1, 3: 2, 4: 2, 5: 1, 6: 1, 7: 2, 8: 3, 9: 3}
+FOLDED_LAUNCHES = {1: 3, 2: 1, 3: 2, 4: 2, 5: 3, 6: 2, 7: 4, 8: 3, 9: 3}
 # configs whose E (intersected elements) the generic executor's
 # metering pass measures in seconds; the others report count time only
 METERED_CONFIGS = ("cfg1", "cfg2")

@@ -48,9 +48,11 @@ extern "C" {
 
 /* flags argument of the count calls */
 #define SMG_METER 1u /* also compute E, the intersected-element count */
-/* Run the generic plan executor even where a folded closed-form kernel exists
- * for the plan (the folded kernels, tindex.cu, never meter E: SMG_METER also
- * selects the generic executor).  For A/B parity checks. */
+/* Run the generic plan executor, on the caller's vertex labels, even where a
+ * folded closed-form kernel exists for the plan or its full count is
+ * label-free (clique plans and the 4-vertex closed forms otherwise run on a
+ * degree-ordered copy of the CSR).  The folded kernels never meter E:
+ * SMG_METER also selects this path.  For A/B parity checks. */
 #define SMG_GENERIC 2u
 /* Root-range calls (smg_count_range) of the two-centre folded kinds (house,
  * tailed diamond b, path4, rectangle) run the generic executor unless this
@@ -156,6 +158,17 @@ int smg_plan_describe(const smg_plan* plan, char* buf, size_t cap);
  */
 int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint32_t flags,
               smg_result* out);
+
+/*
+ * motif_counts' loop over plans (engine.cpp:193-205: one count_instances per
+ * connected pattern) as one call: out[i] is what smg_count(g, &plans[i],
+ * num_gpus, flags, &out[i]) returns.  Work the plans share is done once per
+ * call: the 4-vertex plans that have a closed form over subgraph counts of the
+ * whole graph (star, path, cycle, tailed triangle, diamond) share one 4-clique
+ * count, one triangle-per-edge pass and one 4-cycle pass.
+ */
+int smg_count_many(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, unsigned num_gpus,
+                   uint32_t flags, smg_result* out);
 
 /*
  * One shard of the level-1 units on replica `replica` of g (one process per

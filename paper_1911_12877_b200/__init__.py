@@ -12,14 +12,14 @@ and executes it with hand-written CUDA for sm_100a:
     count(g, named_plan("triangle"))        # -> 4
 """
 from ._native import CountOverflowError, InputError, IoError
-from .engine import (CountResult, count, count_pattern, count_range, count_result, count_shard,
+from .engine import (CountResult, count, count_many, count_pattern, count_range, count_result, count_shard,
                      device_count, enumerate, motif_counts)
 from .graph import Graph
 from .plan import Plan, PlanLevel, compile_plan, motif_plans, named_plan
 
 __all__ = [
     "CountOverflowError", "CountResult", "Graph", "InputError", "IoError", "Plan", "PlanLevel",
-    "compile_plan", "count", "count_pattern", "count_range", "count_result", "count_shard",
+    "compile_plan", "count", "count_many", "count_pattern", "count_range", "count_result", "count_shard",
     "device_count", "enumerate", "motif_counts", "motif_plans", "named_plan",
 ]
 

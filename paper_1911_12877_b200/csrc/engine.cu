@@ -2329,7 +2329,6 @@ struct Replica {
   DevCSR ocsr;
   bool view_oriented = false;                          // off/adj/src currently point at ocsr
   bool map_oriented = false;                           // labelling the cached shard map belongs to
-  double post_extra_ms = 0;                            // device time of sub-counts finish() adds
   std::mutex mu;
 };
 
@@ -2885,14 +2884,15 @@ struct OrientedView {
   OrientedView& operator=(const OrientedView&) = delete;
 };
 
-// 1: clique plan (generic executor on the oriented view); 2: rectangle kinds
-// (c4_launch); 0: keep the caller's labelling.
+// 1: clique plan (generic executor on the oriented view); 2: the 4-vertex
+// kinds with a closed form over subgraph counts (m4_launch); 0: keep the
+// caller's labelling.
 int relabel_mode(const smg_plan& plan, uint32_t flags) {
   if (!g_relabel || (flags & (SMG_METER | SMG_GENERIC))) return 0;
   if (clique_plan(plan)) return 1;
   if (!g_fast) return 0;
-  const int k = fast_kind(plan);
-  return (k == kFastRectangle || k == kFastRectangleMotif) ? 2 : 0;
+  M4Weights w;
+  return m4_weights(fast_kind(plan), &w) ? 2 : 0;
 }
 
 int enqueue_oriented(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
@@ -2902,15 +2902,29 @@ int enqueue_oriented(const smg_graph& g, Replica& r, const Program& prog, const 
   return enqueue(g, r, prog, L);
 }
 
-// Induced 4-cycles of the whole graph (both rectangle plans), this shard's
-// share: C4 - D over the shard's centres / slot chunks (c4_launch) + 3 x the
-// shard's share of the 4-clique count.
-int enqueue_c4(const smg_graph& g, Replica& r, int kind, const Launch& L) {
+// Full counts of 4-vertex kinds as weighted sums of subgraph counts of the
+// whole graph (tindex.cu, m4_launch), this shard's shares: one 4-clique count
+// (generic executor), one set of passes over the shard's vertices / edges,
+// then each plan's weights on the host.  Synchronous.  Caller holds r.mu.
+struct M4Out {
+  __int128 share = 0;
+  uint64_t units = 0;
+  double ms = 0;
+};
+
+int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* const* plans, uint32_t np,
+             const Launch& L, M4Out* out) {
   r.post_kind = 0;
-  r.post_extra_ms = 0;
   int rc = ensure_oriented(g, r);
   if (rc) return rc;
   OrientedView view(r);
+  M4Weights W[16];
+  if (np == 0 || np > 16) return fail(SMG_EINPUT, "bad plan count");
+  unsigned need = 0;
+  for (uint32_t i = 0; i < np; ++i) {
+    if (!m4_weights(kinds[i], &W[i])) return fail(SMG_EIO, "internal: kind has no closed form");
+    need |= W[i].need();
+  }
   // K4 share: the clique plan v0 > v1 > v2 > v3 through the generic executor
   unsigned long long k4 = 0;
   double k4_ms = 0;
@@ -2941,7 +2955,9 @@ int enqueue_c4(const smg_graph& g, Replica& r, int kind, const Launch& L) {
   }
   cudaStream_t st = r.active();
   const unsigned blocks = static_cast<unsigned>(r.num_sms) * 2;
-  const size_t dense_need = static_cast<size_t>(blocks) * std::max<uint64_t>(g.n, 1) * sizeof(uint32_t);
+  const size_t dense_need = (need & (1u << kM4C4))
+                                ? static_cast<size_t>(blocks) * std::max<uint64_t>(g.n, 1) * sizeof(uint32_t)
+                                : 0;
   if (dense_need > r.fast_dense_bytes) {
     if (r.fast_dense) cudaFree(r.fast_dense);
     r.fast_dense = nullptr;
@@ -2950,7 +2966,7 @@ int enqueue_c4(const smg_graph& g, Replica& r, int kind, const Launch& L) {
     SMG_CUDA(cudaMemsetAsync(r.fast_dense, 0, dense_need, st));
     r.fast_dense_bytes = dense_need;
   }
-  const size_t words = 4 * static_cast<size_t>(blocks);
+  const size_t words = 2 * static_cast<size_t>(kM4Regions) * blocks;
   if (words > r.part_words) {
     if (r.part_dev) cudaFree(r.part_dev);
     if (r.part_host) cudaFreeHost(r.part_host);
@@ -2963,6 +2979,19 @@ int enqueue_c4(const smg_graph& g, Replica& r, int kind, const Launch& L) {
   }
   FastArgs a;
   std::memset(&a, 0, sizeof(a));
+  if (need & (1u << kM4Paw)) {  // per-vertex triangle sums live in the per-slot accumulator buffer
+    const size_t acc_need = std::max<uint64_t>(g.n, 1) * sizeof(unsigned long long);
+    if (acc_need > r.fast_acc_bytes) {
+      if (r.fast_acc) cudaFree(r.fast_acc);
+      r.fast_acc = nullptr;
+      r.fast_acc_bytes = 0;
+      SMG_CUDA(cudaMalloc(&r.fast_acc, acc_need));
+      r.fast_acc_bytes = acc_need;
+    }
+    r.fast_acc_kind = 0;  // whatever pass it cached is overwritten
+    SMG_CUDA(cudaMemsetAsync(r.fast_acc, 0, acc_need, st));
+    a.acc0 = r.fast_acc;
+  }
   a.off = r.off;
   a.adj = r.adj;
   a.src = r.src;
@@ -2972,6 +3001,7 @@ int enqueue_c4(const smg_graph& g, Replica& r, int kind, const Launch& L) {
   a.e_hi = g.slots;
   a.num_shards = L.num_shards;
   a.shard = L.shard;
+  a.units_per_edge = 1;
   a.dmax = g.max_degree;
   a.dense = r.fast_dense;
   a.part = r.part_dev;
@@ -2982,18 +3012,44 @@ int enqueue_c4(const smg_graph& g, Replica& r, int kind, const Launch& L) {
   a.overflow = &r.ctr->overflow;
   SMG_CUDA(cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st));
   SMG_CUDA(cudaEventRecord(r.ev0, st));
-  if (g.slots && c4_launch(a, blocks, st)) return fail(SMG_EIO, "4-cycle kernel launch failed");
-  SMG_CUDA(cudaMemcpyAsync(r.part_host, r.part_dev, 4 * blocks * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
+  if (g.slots && m4_launch(a, need, blocks, st)) return fail(SMG_EIO, "4-vertex closed-form kernel launch failed");
   SMG_CUDA(cudaGetLastError());
   SMG_CUDA(cudaEventRecord(r.ev1, st));
+  SMG_CUDA(cudaMemcpyAsync(r.part_host, r.part_dev, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   SMG_CUDA(cudaMemcpyAsync(r.host_ctr, r.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-  r.post_kind = kind;
-  r.post_blocks = blocks;
-  r.post_global = static_cast<__int128>(k4) * 3;
-  r.post_extra_ms = k4_ms;
-  if (!g.slots) std::memset(r.part_host, 0, 4 * blocks * sizeof(unsigned long long));
+  SMG_CUDA(cudaStreamSynchronize(st));
+  float t = 0.f;
+  SMG_CUDA(cudaEventElapsedTime(&t, r.ev0, r.ev1));
+  __int128 S[kM4Regions];
+  for (int q = 0; q < kM4Regions; ++q) {
+    S[q] = 0;
+    if (!g.slots) continue;
+    for (unsigned b = 0; b < blocks; ++b) {
+      const size_t i = 2 * (static_cast<size_t>(q) * blocks + b);
+      S[q] += static_cast<__int128>((static_cast<unsigned __int128>(r.part_host[i + 1]) << 64) | r.part_host[i]);
+    }
+  }
+  if (g_trace)
+    std::fprintf(stderr, "[smg trace] m4 sums: K4=%llu (%.1f ms) C4=%.6g D=%.6g T3=%.6g P4E=%.6g PAW=%.6g STAR=%.6g (%.1f ms)\n",
+                 k4, k4_ms, static_cast<double>(S[kM4C4]), static_cast<double>(S[kM4D]),
+                 static_cast<double>(S[kM4T3]), static_cast<double>(S[kM4P4E]), static_cast<double>(S[kM4Paw]),
+                 static_cast<double>(S[kM4Star]), t);
+  for (uint32_t i = 0; i < np; ++i) {
+    __int128 v = static_cast<__int128>(k4) * W[i].k4;
+    for (int q = 0; q < kM4Regions; ++q) v += S[q] * W[i].w[q];
+    out[i].share = v;
+    out[i].units = r.host_ctr->units * (plans[i]->parent[1] == 0 ? 1u : 2u);
+    out[i].ms = (static_cast<double>(t) + k4_ms) / np;
+  }
   return SMG_OK;
+}
+
+void m4_store(const M4Out& o, smg_result* out) {
+  out->count = static_cast<uint64_t>(o.share);
+  out->count_hi = static_cast<int64_t>(o.share >> 64);
+  out->units = o.units;
+  out->kernel_ms = o.ms;
+  out->per_gpu[0] = out->count;
 }
 
 // The folded kernel for this call, or kFastNone.  range: a root-range call.
@@ -3033,8 +3089,7 @@ int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* 
   *elems = r.host_ctr->elements;
   *units = r.host_ctr->units;
   *ovf = r.host_ctr->overflow != 0;
-  *ms = t + r.post_extra_ms;
-  r.post_extra_ms = 0;
+  *ms = t;
   if (count_hi) *count_hi = 0;
   if (r.post_kind) {
     // centre partials [0, B), ego partials [B, 2B) as (lo, hi) pairs
@@ -3441,14 +3496,19 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
   L.meter_roots = (shard == 0);
   L.shard = shard;
   L.num_shards = num_shards;
-  {
-    const int fk = fast_for(*plan, flags);
-    const int rm = relabel_mode(*plan, flags);
-    rc = rm == 2   ? enqueue_c4(*g, r, fk, L)
-         : rm == 1 ? enqueue_oriented(*g, r, prog, L)
-         : fk      ? enqueue_fast(*g, r, fk, *plan, L)
-                   : enqueue(*g, r, prog, L);
+  const int fk = fast_for(*plan, flags);
+  const int rm = relabel_mode(*plan, flags);
+  if (rm == 2) {
+    M4Out o;
+    rc = m4_count(*g, r, &fk, &plan, 1, L, &o);
+    if (rc) return rc;
+    m4_store(o, out);
+    out->wall_ms = now_ms() - t0;
+    return SMG_OK;
   }
+  rc = rm == 1 ? enqueue_oriented(*g, r, prog, L)
+       : fk    ? enqueue_fast(*g, r, fk, *plan, L)
+               : enqueue(*g, r, prog, L);
   if (rc) return rc;
   bool ovf = false;
   rc = finish(r, &out->count, &out->elements, &out->units, &ovf, &out->kernel_ms, &out->count_hi);
@@ -3606,6 +3666,45 @@ int smg_count_range(const smg_graph* g, const smg_plan* plan, int replica, uint3
   return SMG_OK;
 }
 
+// Shares of `np` 4-vertex closed-form plans on the first num_gpus replicas
+// (one host thread per device; replicas locked by the caller), summed.
+static int m4_count_devices(const smg_graph* g, const int* kinds, const smg_plan* const* plans, uint32_t np,
+                            unsigned num_gpus, smg_result* out) {
+  std::vector<std::vector<M4Out>> res(num_gpus, std::vector<M4Out>(np));
+  std::vector<int> rcs(num_gpus, SMG_OK);
+  std::vector<std::string> errs(num_gpus);
+  auto run = [&](unsigned d) {
+    Launch L;
+    L.unit_begin = 0;
+    L.unit_end = g->slots;
+    L.root_lo = 0;
+    L.root_hi = static_cast<uint32_t>(g->n);
+    L.shard = d;
+    L.num_shards = num_gpus;
+    rcs[d] = m4_count(*g, *g->reps[d], kinds, plans, np, L, res[d].data());
+    if (rcs[d]) errs[d] = g_last_error;  // thread-local: carry it to the caller's thread
+  };
+  std::vector<std::thread> th;
+  for (unsigned d = 1; d < num_gpus; ++d) th.emplace_back(run, d);
+  run(0);
+  for (auto& t : th) t.join();
+  for (unsigned d = 0; d < num_gpus; ++d)
+    if (rcs[d]) return fail(rcs[d], errs[d]);
+  for (uint32_t i = 0; i < np; ++i) {
+    __int128 total = 0;
+    std::memset(&out[i], 0, sizeof(out[i]));
+    for (unsigned d = 0; d < num_gpus; ++d) {
+      total += res[d][i].share;
+      out[i].per_gpu[d] = static_cast<uint64_t>(res[d][i].share);
+      out[i].units += res[d][i].units;
+      out[i].kernel_ms = std::max(out[i].kernel_ms, res[d][i].ms);
+    }
+    if (total < 0 || (total >> 64) != 0) return fail(SMG_EOVERFLOW, "embedding count exceeds 64 bits");
+    out[i].count = static_cast<uint64_t>(total);
+  }
+  return SMG_OK;
+}
+
 int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint32_t flags,
               smg_result* out) {
   const double t0 = now_ms();
@@ -3618,6 +3717,13 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
   if (num_gpus > g->reps.size()) return fail(SMG_EINPUT, "more GPUs requested than graph replicas");
   std::vector<std::unique_lock<std::mutex>> locks;
   for (unsigned d = 0; d < num_gpus; ++d) locks.emplace_back(g->reps[d]->mu);
+  const int fk = fast_for(*plan, flags);
+  const int rm = relabel_mode(*plan, flags);
+  if (rm == 2) {
+    rc = m4_count_devices(g, &fk, &plan, 1, num_gpus, out);
+    out->wall_ms = now_ms() - t0;
+    return rc;
+  }
   for (unsigned d = 0; d < num_gpus; ++d) {
     Launch L;
     L.meter = (flags & SMG_METER) != 0;
@@ -3628,13 +3734,10 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
     L.meter_roots = (d == 0);
     L.shard = d;
     L.num_shards = num_gpus;
-    const int fk = fast_for(*plan, flags);
-    const int rm = relabel_mode(*plan, flags);
     Replica& rd = *g->reps[d];
-    rc = rm == 2   ? enqueue_c4(*g, rd, fk, L)
-         : rm == 1 ? enqueue_oriented(*g, rd, prog, L)
-         : fk      ? enqueue_fast(*g, rd, fk, *plan, L)
-                   : enqueue(*g, rd, prog, L);
+    rc = rm == 1 ? enqueue_oriented(*g, rd, prog, L)
+         : fk    ? enqueue_fast(*g, rd, fk, *plan, L)
+                 : enqueue(*g, rd, prog, L);
     if (rc) {
       // devices 0..d-1 are still counting into their Counters: drain them
       // before the replica locks are released
@@ -3669,6 +3772,55 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
   out->count = static_cast<uint64_t>(total);
   out->wall_ms = now_ms() - t0;
   if (any_ovf) return fail(SMG_EOVERFLOW, "embedding count exceeds 64 bits");
+  return SMG_OK;
+}
+
+// count_instances for a batch of plans on one graph (the motif loop,
+// engine.cpp:193-205): out[i] is what smg_count(g, &plans[i], ...) returns.
+// The 4-vertex plans with a closed form over subgraph counts share one
+// 4-clique count and one set of passes (m4_count); a fully restricted
+// 4-clique plan in the batch takes its count from the same K4.
+int smg_count_many(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, unsigned num_gpus,
+                   uint32_t flags, smg_result* out) {
+  if (!g || !plans || !out) return fail(SMG_EINPUT, "null argument");
+  if (num_gpus == 0) num_gpus = 1;
+  if (num_gpus > g->reps.size()) return fail(SMG_EINPUT, "more GPUs requested than graph replicas");
+  std::vector<int> kinds;
+  std::vector<const smg_plan*> shared;
+  std::vector<uint32_t> idx;
+  for (uint32_t i = 0; i < num_plans; ++i) {
+    Program prog;
+    int rc = prepare(g, &plans[i], &prog);  // validates every plan before any work
+    if (rc) return rc;
+    if (relabel_mode(plans[i], flags) == 2 && shared.size() < 16) {
+      kinds.push_back(fast_kind(plans[i]));
+      shared.push_back(&plans[i]);
+      idx.push_back(i);
+    }
+  }
+  if (shared.size() >= 2) {
+    const double t0 = now_ms();
+    std::vector<smg_result> res(shared.size());
+    {
+      std::vector<std::unique_lock<std::mutex>> locks;
+      for (unsigned d = 0; d < num_gpus; ++d) locks.emplace_back(g->reps[d]->mu);
+      int rc = m4_count_devices(g, kinds.data(), shared.data(), static_cast<uint32_t>(shared.size()), num_gpus,
+                                res.data());
+      if (rc) return rc;
+    }
+    const double wall = now_ms() - t0;
+    for (size_t k = 0; k < shared.size(); ++k) {
+      out[idx[k]] = res[k];
+      out[idx[k]].wall_ms = wall / shared.size();
+    }
+  } else {
+    idx.clear();
+  }
+  for (uint32_t i = 0; i < num_plans; ++i) {
+    if (std::find(idx.begin(), idx.end(), i) != idx.end()) continue;
+    int rc = smg_count(g, &plans[i], num_gpus, flags, &out[i]);
+    if (rc) return rc;
+  }
   return SMG_OK;
 }
 

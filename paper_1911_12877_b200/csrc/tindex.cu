@@ -1072,6 +1072,7 @@ __device__ void store_partial(const FastArgs& a, i128 v, ull units) {
   __shared__ i128 red[kFastThreads / 32];
   __shared__ ull ured[kFastThreads / 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  __syncthreads();  // a kernel may call it once per sum: the previous read of red[] is over
   v = warp_sum128(v);
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) units += __shfl_xor_sync(kAll, units, d);
@@ -1564,38 +1565,50 @@ bool fast_dense(int kind) {
          kind == kFastRectangleMotif;
 }
 
-// ------------------------------------------- induced 4-cycles, full count ---
-// Both rectangle plans count every induced 4-cycle of the graph exactly once
-// (their restrictions leave one of the 8 automorphic embeddings), so the full
-// count does not depend on the vertex labels.  On the degree-ordered copy of
-// the CSR (orient_reindex: id 0 = highest degree; engine.cu keeps one per
-// replica) the count is assembled from three label-free sums:
-//     induced C4 = C4 - D + 3 K4
-//   C4 = sum_c sum_{x > c} C(w_c(x), 2), w_c(x) = #{u in N(c) & N(x) : u > c}:
-//        every 4-cycle (as a subgraph) at its smallest vertex c, opposite x;
-//        only wedges c - u - x with u, x > c are walked, sum_u d(u) d-(u)
-//        elements instead of sum_u d(u)^2 (d- = neighbours of higher degree);
-//   D  = sum_{edges e} C(tri(e), 2): diamonds (K4 minus an edge) as subgraphs,
-//        = induced diamonds + 6 K4;  C4 = induced C4 + induced diamonds + 3 K4;
-//   K4 = the 4-clique count (generic executor, clique-local path).
-// c4_kernel: one CTA per centre c, dense per-CTA table w_c (n words, kept
-// zero between centres).  Each touch adds atomicAdd's return value: the k-th
-// increment of a word returns k - 1, and 0 + 1 + ... + (w - 1) = C(w, 2).
+// ------------------------------- 4-vertex plans, label-free full counts ---
+// Every 4-vertex plan fast_kind() recognises counts each induced instance of
+// its pattern exactly once (its restrictions leave one automorphic embedding),
+// so the full count does not depend on the vertex labels and equals an integer
+// combination of subgraph (non-induced) counts of the whole graph:
+//     K4    = 4-cliques (generic executor, clique-local path)
+//     D     = sum_{edges e} C(t_e, 2)            diamonds,   t_e = |N(u) & N(v)|
+//     C4    = sum_c sum_{x > c} C(w_c(x), 2)     4-cycles,   w_c(x) = #{u in N(c) & N(x) : u > c}
+//     PAW   = sum_v t_v (d_v - 2)                tailed triangles, t_v = triangles at v
+//     P4    = sum_{(u,v) in E} (d_u - 1)(d_v - 1) - 3 T   3-edge paths, T = triangles
+//     S     = sum_v C(d_v, 3)                    3-stars
+//   induced diamond  = D - 6 K4
+//   induced 4-cycle  = C4 - D + 3 K4
+//   induced paw      = PAW - 4 D + 12 K4
+//   induced path4    = P4 - 2 PAW + 6 D - 4 C4 - 12 K4
+//   induced star4    = S - PAW + 2 D - 4 K4
+// (a subgraph copy of X inside an induced Y, counted per Y: paw has 1 star and 2
+// paths; C4 4 paths; diamond 2 stars, 4 paws, 1 C4, 6 paths; K4 4 stars, 12
+// paws, 3 C4, 6 diamonds, 12 paths.)  The sums run on the degree-ordered copy
+// of the CSR (orient_reindex: id 0 = highest degree; engine.cu keeps one per
+// replica): the C4 pass walks only wedges c - u - x with u, x > c, sum_u d(u)
+// d-(u) elements (d- = neighbours of higher degree) instead of sum_u d(u)^2.
+// The kernels store the raw sums per CTA as 128 bits in regions of a.part
+// (kM4* below); the host applies the weights of the kind (m4_weights).
+__device__ __forceinline__ bool owns_vertex(const FastArgs& a, uint32_t v) {
+  return a.num_shards <= 1 || v % a.num_shards == a.shard;
+}
+
+// C4: one CTA per centre c, dense per-CTA table w_c (n words, kept zero between
+// centres).  Each touch adds atomicAdd's return value: the k-th increment of a
+// word returns k - 1, and 0 + 1 + ... + (w - 1) = C(w, 2).
 __global__ void __launch_bounds__(kFastThreads) c4_kernel(const FastArgs a) {
   __shared__ ull center_sh;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint32_t* cnt = a.dense + static_cast<uint64_t>(blockIdx.x) * a.n;
   i128 acc = 0;
-  ull units = 0;
   for (;;) {
     const ull c = next_center(a, &center_sh);
     if (c >= a.n) break;
-    if (a.num_shards > 1 && c % a.num_shards != a.shard) continue;
+    if (!owns_vertex(a, static_cast<uint32_t>(c))) continue;
     const ull co = a.off[c];
     const uint32_t dc = static_cast<uint32_t>(a.off[c + 1] - co);
     const uint32_t k0 = lb32(a.adj + co, dc, static_cast<uint32_t>(c) + 1u);  // first u > c
     const uint32_t np = dc - k0;
-    if (threadIdx.x == 0) units += np;  // level-1 units (v1 < v0): one per undirected edge
     if (np < 2) continue;
     const uint32_t* U = a.adj + co + k0;
     ull s = 0;
@@ -1603,7 +1616,7 @@ __global__ void __launch_bounds__(kFastThreads) c4_kernel(const FastArgs a) {
       const uint32_t u = U[j];
       const ull uo = a.off[u];
       const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
-      // x in N(u), x > c: c itself is in N(u), the suffix starts right after it
+      // x in N(u), x > c (c itself is in N(u): the suffix starts right after it)
       const uint32_t x0 = lb32(a.adj + uo, du, static_cast<uint32_t>(c) + 1u);
       for (uint32_t k = x0 + lane; k < du; k += 32) s += atomicAdd(&cnt[a.adj[uo + k]], 1u);
     }
@@ -1617,26 +1630,31 @@ __global__ void __launch_bounds__(kFastThreads) c4_kernel(const FastArgs a) {
       for (uint32_t k = x0 + lane; k < du; k += 32) cnt[a.adj[uo + k]] = 0u;
     }
   }
-  store_partial(a, acc, units);
+  store_partial(a, acc, 0);
 }
 
-// -D: minus sum over undirected edges (slot e = (u, v), u < v) of C(|N(u) & N(v)|, 2).
-__global__ void __launch_bounds__(kFastThreads) tri_pairs_kernel(const FastArgs a) {
+// Per undirected edge (slot e = (u, v), u < v; the shard that owns u):
+// C(t, 2), t and (d_u - 1)(d_v - 1); and tv[x] += t at the owned endpoints
+// (tv[x] = 2 t_x once every edge at x is in; only when a.acc0 is given).
+__global__ void __launch_bounds__(kFastThreads) m4_edge_kernel(const FastArgs a) {
   const int lane = threadIdx.x & 31;
-  i128 acc = 0;
+  i128 acc_d = 0, acc_t3 = 0, acc_p4 = 0;
+  ull units = 0;
   for (;;) {
     ull chunk = 0;
     if (lane == 0) chunk = atomicAdd(a.next_chunk, 1ull);
     chunk = __shfl_sync(kAll, chunk, 0);
     if (chunk * kSlotChunk >= a.slots) break;
-    if (a.num_shards > 1 && chunk % a.num_shards != a.shard) continue;
     const uint64_t e = chunk * kSlotChunk + lane;
     bool mine = e < a.slots;
     uint32_t u = 0, v = 0;
+    bool own_u = false, own_v = false;
     if (mine) {
       u = a.src[e];
       v = a.adj[e];
-      mine = u < v;
+      own_u = owns_vertex(a, u);
+      own_v = a.acc0 != nullptr && owns_vertex(a, v);
+      mine = u < v && (own_u || own_v);
     }
     ull bu = 0, bv = 0;
     uint32_t du = 0, dv = 0;
@@ -1646,11 +1664,9 @@ __global__ void __launch_bounds__(kFastThreads) tri_pairs_kernel(const FastArgs 
       bv = a.off[v];
       dv = static_cast<uint32_t>(a.off[v + 1] - bv);
     }
+    ull t = 0;
     const bool small = mine && min(du, dv) <= 8;
-    if (small) {
-      const ull t = isect_count(a.adj + bu, du, a.adj + bv, dv);
-      acc -= static_cast<i128>(t * (t - 1) / 2);
-    }
+    if (small) t = isect_count(a.adj + bu, du, a.adj + bv, dv);
     unsigned big = __ballot_sync(kAll, mine && !small);
     while (big) {
       const int j = __ffs(big) - 1;
@@ -1661,30 +1677,95 @@ __global__ void __launch_bounds__(kFastThreads) tri_pairs_kernel(const FastArgs 
       const uint32_t* S = a.adj + (su ? jbu : jbv);
       const uint32_t* L = a.adj + (su ? jbv : jbu);
       const uint32_t ns = su ? jdu : jdv, nl = su ? jdv : jdu;
-      ull t = 0;
+      ull tj = 0;
       for (uint32_t i = lane; i < ns; i += 32) {
         const uint32_t x = S[i];
         const uint32_t p = lb32(L, nl, x);
-        t += (p < nl && L[p] == x) ? 1u : 0u;
+        tj += (p < nl && L[p] == x) ? 1u : 0u;
       }
-      t = warp_sum(t);
-      if (lane == 0) acc -= static_cast<i128>(t * (t - 1) / 2);
+      tj = warp_sum(tj);
+      if (lane == j) t = tj;
+    }
+    if (mine) {
+      if (own_u) {
+        units += a.units_per_edge;
+        acc_d += static_cast<i128>(t * (t - 1) / 2);
+        acc_t3 += static_cast<i128>(t);
+        acc_p4 += static_cast<i128>(static_cast<ull>(du - 1) * static_cast<ull>(dv - 1));
+      }
+      if (a.acc0 != nullptr && t) {
+        if (own_u) atomicAdd(&a.acc0[u], t);
+        if (own_v) atomicAdd(&a.acc0[v], t);
+      }
     }
   }
-  store_partial(a, acc, 0);
+  FastArgs w = a;
+  const unsigned B = gridDim.x;
+  w.part = a.part + 2 * B * kM4D;
+  store_partial(w, acc_d, units);
+  w.part = a.part + 2 * B * kM4T3;
+  store_partial(w, acc_t3, 0);
+  w.part = a.part + 2 * B * kM4P4E;
+  store_partial(w, acc_p4, 0);
 }
 
-// C4 -> part[0 .. blocks), -D -> part[blocks .. 2 blocks) (a.off/adj/src: any
-// labelling of the graph, the degree-ordered one for speed).
-int c4_launch(const FastArgs& a, unsigned blocks, cudaStream_t st) {
-  if (cudaMemsetAsync(a.part, 0, 4 * blocks * sizeof(ull), st) != cudaSuccess) return 1;
-  if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
-  c4_kernel<<<blocks, kFastThreads, 0, st>>>(a);
-  if (cudaGetLastError() != cudaSuccess) return 1;
+// Per owned vertex v: (d_v - 2) t_v and C(d_v, 3), t_v = tv[v] / 2 (0 when
+// a.acc0 is not given); tv is zeroed again.
+__global__ void __launch_bounds__(kFastThreads) m4_vertex_kernel(const FastArgs a) {
+  i128 acc_paw = 0, acc_star = 0;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < a.n;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (!owns_vertex(a, static_cast<uint32_t>(v))) continue;
+    const ull d = a.off[v + 1] - a.off[v];
+    if (d >= 3) acc_star += static_cast<i128>(d * (d - 1) / 2) * static_cast<i128>(d - 2) / 3;
+    if (a.acc0 != nullptr) {
+      const ull tv = a.acc0[v] / 2;
+      a.acc0[v] = 0ull;
+      if (tv) acc_paw += static_cast<i128>(tv) * static_cast<i128>(d - 2);
+    }
+  }
   FastArgs w = a;
-  w.part = a.part + 2 * blocks;
-  tri_pairs_kernel<<<blocks, kFastThreads, 0, st>>>(w);
-  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+  const unsigned B = gridDim.x;
+  w.part = a.part + 2 * B * kM4Paw;
+  store_partial(w, acc_paw, 0);
+  w.part = a.part + 2 * B * kM4Star;
+  store_partial(w, acc_star, 0);
+}
+
+// need: bit r set = region r (kM4*) is wanted.  a.part: kM4Regions x blocks pairs.
+int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st) {
+  if (cudaMemsetAsync(a.part, 0, 2 * kM4Regions * blocks * sizeof(ull), st) != cudaSuccess) return 1;
+  if (need & (1u << kM4C4)) {
+    if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
+    FastArgs w = a;
+    w.part = a.part + 2 * blocks * kM4C4;
+    c4_kernel<<<blocks, kFastThreads, 0, st>>>(w);
+    if (cudaGetLastError() != cudaSuccess) return 1;
+  }
+  FastArgs w = a;
+  if (!(need & (1u << kM4Paw))) w.acc0 = nullptr;  // no per-vertex triangle counts needed
+  m4_edge_kernel<<<blocks, kFastThreads, 0, st>>>(w);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  if (need & ((1u << kM4Paw) | (1u << kM4Star))) {
+    m4_vertex_kernel<<<blocks, kFastThreads, 0, st>>>(w);
+    if (cudaGetLastError() != cudaSuccess) return 1;
+  }
+  return 0;
+}
+
+bool m4_weights(int kind, M4Weights* w) {
+  *w = M4Weights{};
+  switch (kind) {
+    case kFastRectangle:
+    case kFastRectangleMotif: w->w[kM4C4] = 1; w->w[kM4D] = -1; w->k4 = 3; return true;
+    case kFastDiamond: w->w[kM4D] = 1; w->k4 = -6; return true;
+    case kFastTailedTriangle: w->w[kM4Paw] = 1; w->w[kM4D] = -4; w->k4 = 12; return true;
+    case kFastPath4:
+      w->w[kM4P4E] = 1; w->w[kM4T3] = -1; w->w[kM4Paw] = -2; w->w[kM4D] = 6; w->w[kM4C4] = -4; w->k4 = -12;
+      return true;
+    case kFastStar4: w->w[kM4Star] = 1; w->w[kM4Paw] = -1; w->w[kM4D] = 2; w->k4 = -4; return true;
+    default: return false;
+  }
 }
 
 bool fast_has_full(int kind) {

@@ -51,7 +51,8 @@ struct FastArgs {
   uint64_t e_lo, e_hi;                 // slots the unit kernels walk ([0, slots), or off[lo]..off[hi])
   int via_rev;                         // the unit's own slot is the reverse of the walked one
   uint32_t num_shards;                 // > 1: shard map below
-  uint32_t shard;                      // this shard (c4_launch: centres / chunks dealt round-robin)
+  uint32_t shard;                      // this shard (m4_launch: vertices dealt round-robin)
+  uint32_t units_per_edge;             // m4_launch: level-1 units per undirected edge (1: v1 < v0, else 2)
   const unsigned long long* map_begin;
   const unsigned long long* map_pref;
   uint32_t map_k;
@@ -88,11 +89,26 @@ int fast_launch(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st, b
 // when launched, 2 when the kind has no full mode.
 int fast_launch_full(int kind, const FastArgs& a, unsigned blocks, cudaStream_t st);
 bool fast_has_full(int kind);
-// Induced 4-cycle full count, label-free form (see tindex.cu): C4 partials ->
-// a.part[0 .. 2 blocks), -D partials -> a.part[2 blocks .. 4 blocks); the
-// caller adds 3 K4.  Needs a.dense (blocks x n words, zero), a.next2,
-// a.next_chunk (zeroed), a.off/adj/src of the (degree-ordered) CSR.
-int c4_launch(const FastArgs& a, unsigned blocks, cudaStream_t st);
+// 4-vertex kinds, label-free full counts (see tindex.cu): integer combinations
+// of subgraph counts of the whole graph.  m4_launch stores the raw sums, per
+// CTA as 128-bit pairs, in regions of a.part (kM4Regions x blocks pairs); the
+// host applies the kind's weights (m4_weights; false: no such form) and adds
+// k4 x the 4-clique count.  Needs a.dense (blocks x n words, zero; C4 wanted),
+// a.acc0 (n words, zero; PAW wanted), a.next2 / a.next_chunk (zeroed) and
+// a.off/adj/src of the (degree-ordered) CSR.
+enum M4Region { kM4C4 = 0, kM4D = 1, kM4T3 = 2, kM4P4E = 3, kM4Paw = 4, kM4Star = 5, kM4Regions = 6 };
+struct M4Weights {
+  int w[kM4Regions] = {0, 0, 0, 0, 0, 0};
+  int k4 = 0;
+  unsigned need() const {
+    unsigned m = 0;
+    for (int r = 0; r < kM4Regions; ++r)
+      if (w[r]) m |= 1u << r;
+    return m;
+  }
+};
+bool m4_weights(int kind, M4Weights* w);
+int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st);
 // Sum over index entries of k4 * (k4 - 1) (every entry of the index; needs
 // the k4 array).  Synchronous.
 int tindex_k4_pairs(const TIndex& t, int num_sms, cudaStream_t st, unsigned long long* out, std::string* err);

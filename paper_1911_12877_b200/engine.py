@@ -74,12 +74,27 @@ def count_pattern(graph: Graph, name: str, k: int = 0, gpus: int = 1) -> int:
     return count(graph, named_plan(name, k), gpus)
 
 
+def count_many(graph: Graph, plans, gpus: int = 1, generic: bool = False) -> list[CountResult]:
+    """One count_instances per plan, as one call (smg_count_many): work the
+    plans share (the 4-clique count, triangle-per-edge and 4-cycle passes of
+    the 4-vertex closed forms) is done once."""
+    ps = [_plan(p) for p in plans]
+    gpus = max(1, int(gpus))
+    lib = N.gpu_lib()
+    h = graph.device_handle(tuple(range(gpus)))
+    arr = (N.SmgPlan * max(1, len(ps)))(*[p.to_smg() for p in ps])
+    res = (N.SmgResult * max(1, len(ps)))()
+    N.check_gpu(lib.smg_count_many(h, arr, len(ps), gpus, _flags(False, generic), res))
+    return [_result(res[i], gpus) for i in range(len(ps))]
+
+
 def motif_counts(graph: Graph, k: int, gpus: int = 1) -> list[dict]:
-    out = []
-    for rec in motif_plans(k):
-        out.append({"bits": rec["bits"], "name": rec["name"], "key": rec["key"],
-                    "count": count(graph, rec["plan"], gpus)})
-    return out
+    """motif_counts (engine.cpp:193-205): every connected k-vertex pattern with
+    its own plan, counted in one smg_count_many call."""
+    recs = motif_plans(k)
+    res = count_many(graph, [rec["plan"] for rec in recs], gpus)
+    return [{"bits": rec["bits"], "name": rec["name"], "key": rec["key"], "count": r.count}
+            for rec, r in zip(recs, res)]
 
 
 def count_range(graph: Graph, plan, lo: int, hi: int, device: int = 0, meter: bool = False,

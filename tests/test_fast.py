@@ -122,3 +122,26 @@ def test_label_free_full_counts(spec, port):
         assert count_result(go, plan).count == c, name
         for s in (2, 5):
             assert sum(count_shard(g, plan, i, s).count for i in range(s)) == c, (name, s)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", [configs.GraphSpec("rmat", (13, 12, 0.57, 0.19, 0.19), 31),
+                                  configs.GraphSpec("chung_lu", (6000, 60000, 2.1, 600.0), 12)],
+                         ids=lambda s: s.tag)
+def test_count_many_shares_work_and_matches_single_counts(spec, port):
+    """smg_count_many (the motif loop, engine.cpp:193-205, as one call): every
+    result equals the plan's own smg_count and the oracle; motif_counts goes
+    through it."""
+    from paper_1911_12877_b200 import count_many, motif_counts
+    g = configs.load(spec)
+    recs = motif_plans(4)
+    plans = [r["plan"] for r in recs] + [named_plan("house"), named_plan("triangle"), named_plan("rectangle")]
+    many = count_many(g, plans)
+    for plan, r in zip(plans, many):
+        single = count_result(g, plan)
+        c, _ = port.count(g.offsets, g.adjacency, plan.to_smg(), threads=8)
+        assert r.count == single.count == c
+        assert r.units == single.units
+    assert [m["count"] for m in motif_counts(g, 4)] == [r.count for r in many[: len(recs)]]
+    two = count_many(g, plans, gpus=1, generic=True)
+    assert [r.count for r in two] == [r.count for r in many]
