@@ -364,6 +364,15 @@ def our_arm(args):
                                         N.SMG_METER if meter else 0, ctypes.byref(r)))
         return r
 
+    plan_arr = (N.SmgPlan * len(plans))(*[p.to_smg() for _, p in plans])
+
+    def step(handle):
+        """One step: this rank's shard of every pattern of the config, one
+        smg_count_many_shard call (work the plans share is done once per call)."""
+        res = (N.SmgResult * len(plans))()
+        N.check_gpu(lib.smg_count_many_shard(handle, plan_arr, len(plans), 0, rank, world, 0, res))
+        return res
+
     # metering pass: E per pattern (deterministic property of graph + plan).
     # Plans that lower to a folded closed-form kernel (csrc/tindex.cu) never
     # enumerate the merges E counts; a config with one reports count time.
@@ -372,7 +381,7 @@ def our_arm(args):
     E, counts = {}, {}
     for label, plan in plans:
         r = shard(plan, meter=metered)
-        c, e = allsum_u64([r.count, r.elements])
+        c, e = allsum_u64([(int(r.count_hi) << 64) + int(r.count), r.elements])
         E[label], counts[label] = (e if metered else None), c
     E_total = sum(E.values()) if metered else None
 
@@ -381,8 +390,7 @@ def our_arm(args):
           for _ in range(args.steps)]
     kern_ms = {label: [] for label, _ in plans}
     for _ in range(args.warmup):
-        for label, plan in plans:
-            shard(plan)
+        step(h)
         flush.add_(1)
     torch.cuda.synchronize(dev)
     barrier()
@@ -392,11 +400,10 @@ def our_arm(args):
         for s in range(args.steps):
             flush.add_(1)  # L2 flush between timed steps (outside the events)
             ev[s][0].record(stream)
-            cs = []
-            for label, plan in plans:
-                r = shard(plan)
-                kern_ms[label].append(r.kernel_ms)
-                cs.append(r.count)
+            res = step(h)
+            cs = [(int(res[i].count_hi) << 64) + int(res[i].count) for i in range(len(plans))]
+            for i, (label, _) in enumerate(plans):
+                kern_ms[label].append(res[i].kernel_ms)
             ev[s][1].record(stream)
             step_counts.append(cs)
         torch.cuda.synchronize(dev)
@@ -425,12 +432,8 @@ def our_arm(args):
         N.check_gpu(lib.smg_graph_create(ctypes.cast(off_pin.data_ptr(), ctypes.POINTER(ctypes.c_uint64)),
                                          ctypes.cast(adj_pin.data_ptr(), ctypes.POINTER(ctypes.c_uint32)),
                                          graph.n, dev_arr, 1, ctypes.byref(gh)))
-        cs = []
-        for label, plan in plans:
-            sp = plan.to_smg()
-            r = N.SmgResult()
-            N.check_gpu(lib.smg_count_shard(gh, ctypes.byref(sp), 0, rank, world, 0, ctypes.byref(r)))
-            cs.append(r.count)
+        res = step(gh)
+        cs = [int(res[i].count) for i in range(len(plans))]
         lib.smg_graph_destroy(gh)
         dt = time.perf_counter() - t0
         if s > 0:  # first iteration warms the allocator / context

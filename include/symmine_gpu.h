@@ -165,10 +165,15 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
  * num_gpus, flags, &out[i]) returns.  Work the plans share is done once per
  * call: the 4-vertex plans that have a closed form over subgraph counts of the
  * whole graph (star, path, cycle, tailed triangle, diamond) share one 4-clique
- * count, one triangle-per-edge pass and one 4-cycle pass.
+ * count, one triangle-per-edge pass and one 4-cycle pass, and a fully
+ * restricted 4-clique plan in the batch takes its count from the same K4.
  */
 int smg_count_many(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, unsigned num_gpus,
                    uint32_t flags, smg_result* out);
+/* The same for one shard on one replica (one process per GPU): out[i] is what
+ * smg_count_shard(g, &plans[i], replica, shard, num_shards, flags, &out[i]) returns. */
+int smg_count_many_shard(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, int replica,
+                         uint32_t shard, uint32_t num_shards, uint32_t flags, smg_result* out);
 
 /*
  * One shard of the level-1 units on replica `replica` of g (one process per

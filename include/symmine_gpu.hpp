@@ -169,4 +169,24 @@ inline CountResult count_instances(const Graph& g, const Plan& plan, unsigned gp
   return out;
 }
 
+// One count_instances per plan as one call (the loop of motif_counts,
+// engine.cpp:193-205): work the plans share on the device is done once.
+inline std::vector<CountResult> count_many(const Graph& g, const std::vector<Plan>& plans, unsigned gpus = 1) {
+  if (gpus == 0) gpus = 1;
+  std::vector<smg_plan> pods;
+  pods.reserve(plans.size());
+  for (const Plan& p : plans) pods.push_back(detail::lower(p));
+  std::vector<smg_result> res(plans.size());
+  if (!plans.empty())
+    detail::check(smg_count_many(detail::replica(g, gpus), pods.data(), static_cast<uint32_t>(pods.size()), gpus, 0,
+                                 res.data()));
+  std::vector<CountResult> out(plans.size());
+  for (size_t i = 0; i < plans.size(); ++i) {
+    out[i].count = res[i].count;
+    out[i].per_worker.assign(res[i].per_gpu, res[i].per_gpu + gpus);
+    out[i].wall_ms = res[i].wall_ms;
+  }
+  return out;
+}
+
 }  // namespace symmine::gpu

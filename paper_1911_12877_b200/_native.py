@@ -115,6 +115,9 @@ def gpu_lib():
             _bind(lib, "smg_count_many", ctypes.c_int,
                   [_P, ctypes.POINTER(SmgPlan), ctypes.c_uint32, ctypes.c_uint, ctypes.c_uint32,
                    ctypes.POINTER(SmgResult)])
+            _bind(lib, "smg_count_many_shard", ctypes.c_int,
+                  [_P, ctypes.POINTER(SmgPlan), ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
+                   ctypes.c_uint32, ctypes.POINTER(SmgResult)])
             _bind(lib, "smg_count_shard", ctypes.c_int,
                   [_P, ctypes.POINTER(SmgPlan), ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
                    ctypes.c_uint32, ctypes.POINTER(SmgResult)])

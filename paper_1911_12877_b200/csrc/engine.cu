@@ -3775,33 +3775,59 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
   return SMG_OK;
 }
 
-// count_instances for a batch of plans on one graph (the motif loop,
-// engine.cpp:193-205): out[i] is what smg_count(g, &plans[i], ...) returns.
-// The 4-vertex plans with a closed form over subgraph counts share one
-// 4-clique count and one set of passes (m4_count); a fully restricted
-// 4-clique plan in the batch takes its count from the same K4.
-int smg_count_many(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, unsigned num_gpus,
-                   uint32_t flags, smg_result* out) {
+// The batch kind of a plan inside smg_count_many: a 4-vertex closed-form kind,
+// kFastClique4 for a fully restricted 4-clique plan (its count is the K4 the
+// closed forms need anyway), or 0 (counted on its own).
+static int batch_kind(const smg_plan& p, uint32_t flags) {
+  if (relabel_mode(p, flags) == 2) return fast_kind(p);
+  if (!g_relabel || !g_fast || (flags & (SMG_METER | SMG_GENERIC))) return 0;
+  if (p.depth == 4 && clique_plan(p) && p.parent[1] == 0 && p.parent[2] == 1 && p.parent[3] == 2) return kFastClique4;
+  return 0;
+}
+
+// shard_mode: one shard on one replica (smg_count_many_shard), else the first
+// num_gpus replicas (smg_count_many).
+static int count_many_impl(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, bool shard_mode,
+                           int replica, uint32_t shard, uint32_t num_shards, unsigned num_gpus, uint32_t flags,
+                           smg_result* out) {
   if (!g || !plans || !out) return fail(SMG_EINPUT, "null argument");
-  if (num_gpus == 0) num_gpus = 1;
-  if (num_gpus > g->reps.size()) return fail(SMG_EINPUT, "more GPUs requested than graph replicas");
   std::vector<int> kinds;
   std::vector<const smg_plan*> shared;
   std::vector<uint32_t> idx;
+  bool closed_form = false;
   for (uint32_t i = 0; i < num_plans; ++i) {
     Program prog;
     int rc = prepare(g, &plans[i], &prog);  // validates every plan before any work
     if (rc) return rc;
-    if (relabel_mode(plans[i], flags) == 2 && shared.size() < 16) {
-      kinds.push_back(fast_kind(plans[i]));
+    const int k = batch_kind(plans[i], flags);
+    if (k && shared.size() < 16) {
+      kinds.push_back(k);
       shared.push_back(&plans[i]);
       idx.push_back(i);
+      closed_form |= k != kFastClique4;
     }
   }
-  if (shared.size() >= 2) {
+  if (shared.size() >= 2 && closed_form) {
     const double t0 = now_ms();
     std::vector<smg_result> res(shared.size());
-    {
+    if (shard_mode) {
+      Replica& r = *g->reps[replica];
+      std::lock_guard<std::mutex> lock(r.mu);
+      Launch L;
+      L.unit_begin = 0;
+      L.unit_end = g->slots;
+      L.root_lo = 0;
+      L.root_hi = static_cast<uint32_t>(g->n);
+      L.shard = shard;
+      L.num_shards = num_shards;
+      std::vector<M4Out> o(shared.size());
+      int rc = m4_count(*g, r, kinds.data(), shared.data(), static_cast<uint32_t>(shared.size()), L, o.data());
+      if (rc) return rc;
+      for (size_t k = 0; k < shared.size(); ++k) {
+        std::memset(&res[k], 0, sizeof(res[k]));
+        m4_store(o[k], &res[k]);
+      }
+    } else {
       std::vector<std::unique_lock<std::mutex>> locks;
       for (unsigned d = 0; d < num_gpus; ++d) locks.emplace_back(g->reps[d]->mu);
       int rc = m4_count_devices(g, kinds.data(), shared.data(), static_cast<uint32_t>(shared.size()), num_gpus,
@@ -3818,10 +3844,34 @@ int smg_count_many(const smg_graph* g, const smg_plan* plans, uint32_t num_plans
   }
   for (uint32_t i = 0; i < num_plans; ++i) {
     if (std::find(idx.begin(), idx.end(), i) != idx.end()) continue;
-    int rc = smg_count(g, &plans[i], num_gpus, flags, &out[i]);
+    int rc = shard_mode ? smg_count_shard(g, &plans[i], replica, shard, num_shards, flags, &out[i])
+                        : smg_count(g, &plans[i], num_gpus, flags, &out[i]);
     if (rc) return rc;
   }
   return SMG_OK;
+}
+
+// count_instances for a batch of plans on one graph (the motif loop,
+// engine.cpp:193-205): out[i] is what smg_count(g, &plans[i], ...) returns.
+// The 4-vertex plans with a closed form over subgraph counts share one
+// 4-clique count and one set of passes (m4_count); a fully restricted
+// 4-clique plan in the batch takes its count from the same K4.
+int smg_count_many(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, unsigned num_gpus,
+                   uint32_t flags, smg_result* out) {
+  if (!g) return fail(SMG_EINPUT, "null graph");
+  if (num_gpus == 0) num_gpus = 1;
+  if (num_gpus > g->reps.size()) return fail(SMG_EINPUT, "more GPUs requested than graph replicas");
+  return count_many_impl(g, plans, num_plans, false, 0, 0, 1, num_gpus, flags, out);
+}
+
+// The same for one shard on one replica (one process per GPU): out[i] is what
+// smg_count_shard(g, &plans[i], replica, shard, num_shards, ...) returns.
+int smg_count_many_shard(const smg_graph* g, const smg_plan* plans, uint32_t num_plans, int replica,
+                         uint32_t shard, uint32_t num_shards, uint32_t flags, smg_result* out) {
+  if (!g) return fail(SMG_EINPUT, "null graph");
+  if (replica < 0 || replica >= static_cast<int>(g->reps.size())) return fail(SMG_EINPUT, "bad replica");
+  if (num_shards == 0 || shard >= num_shards) return fail(SMG_EINPUT, "bad shard");
+  return count_many_impl(g, plans, num_plans, true, replica, shard, num_shards, 1, flags, out);
 }
 
 }  // extern "C"

@@ -1764,6 +1764,7 @@ bool m4_weights(int kind, M4Weights* w) {
       w->w[kM4P4E] = 1; w->w[kM4T3] = -1; w->w[kM4Paw] = -2; w->w[kM4D] = 6; w->w[kM4C4] = -4; w->k4 = -12;
       return true;
     case kFastStar4: w->w[kM4Star] = 1; w->w[kM4Paw] = -1; w->w[kM4D] = 2; w->k4 = -4; return true;
+    case kFastClique4: w->k4 = 1; return true;
     default: return false;
   }
 }

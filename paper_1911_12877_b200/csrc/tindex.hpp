@@ -38,7 +38,8 @@ void tindex_free(TIndex* t);
 // leaves fold into closed forms over the ego network of v1 (tindex.cu).
 enum FastKind {
   kFastNone = 0, kFastStar4 = 1, kFastTailedDiamondA = 2, kFastHouse = 3, kFastTailedDiamondB = 4,
-  kFastTailedTriangle = 5, kFastDiamond = 6, kFastPath4 = 7, kFastRectangle = 8, kFastRectangleMotif = 9
+  kFastTailedTriangle = 5, kFastDiamond = 6, kFastPath4 = 7, kFastRectangle = 8, kFastRectangleMotif = 9,
+  kFastClique4 = 10  // never returned by fast_kind: a fully restricted 4-clique plan inside a batch (m4_weights)
 };
 int fast_kind(const smg_plan& p);
 

@@ -40,6 +40,22 @@ int main() {
       if (cpu != r.count) ++bad;
     }
   }
+  // the motif loop (engine.cpp:193-205) as one batched call
+  {
+    std::vector<Plan> plans;
+    std::vector<uint64_t> cpu;
+    for (Pattern& p : connected_patterns(4)) {
+      const SelectedSchedule sel = select_schedule(p, {});
+      plans.push_back(compile_plan(p, sel.choice.schedule, sel.choice.restrictions));
+      cpu.push_back(count_instances(g, plans.back(), 4).count);
+    }
+    const std::vector<CountResult> many = gpu::count_many(g, plans, 1);
+    for (size_t i = 0; i < plans.size(); ++i) {
+      std::printf("motif4[%zu] cpu=%llu gpu(count_many)=%llu\n", i, (unsigned long long)cpu[i],
+                  (unsigned long long)many[i].count);
+      if (cpu[i] != many[i].count) ++bad;
+    }
+  }
   // errors cross the ABI as the reference's exception types
   Plan broken = compile_plan(named_pattern("triangle"), {0, 1, 2}, {-1, 0, 1});
   broken.levels[2].restriction_parent = 2;

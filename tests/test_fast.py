@@ -145,3 +145,12 @@ def test_count_many_shares_work_and_matches_single_counts(spec, port):
     assert [m["count"] for m in motif_counts(g, 4)] == [r.count for r in many[: len(recs)]]
     two = count_many(g, plans, gpus=1, generic=True)
     assert [r.count for r in two] == [r.count for r in many]
+    # one shard per process: smg_count_many_shard shares sum to the totals
+    import ctypes
+    sm = (N.SmgPlan * len(plans))(*[p.to_smg() for p in plans])
+    tot = [0] * len(plans)
+    for i in range(3):
+        res = (N.SmgResult * len(plans))()
+        N.check_gpu(N.gpu_lib().smg_count_many_shard(g.device_handle((0,)), sm, len(plans), 0, i, 3, 0, res))
+        tot = [t + (int(res[k].count_hi) << 64) + int(res[k].count) for k, t in enumerate(tot)]
+    assert tot == [r.count for r in many]
