@@ -275,16 +275,28 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_profile(cfg, label):
-    """ncu figures (DRAM bytes per count, L2 hit rate) of the dominant count,
-    from the committed summary of this workload (profiles/ncu_summary.json)."""
+def load_profile(cfg, kernel):
+    """ncu figures (DRAM bytes per step, L2 hit rate) of one kernel of this
+    config's step, from the committed summary (profiles/ncu_summary.json,
+    written by tools/traffic_summary.py).  The c4 phase sums c4_kernel and the
+    c4_hub_kernel launches."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
     except Exception:
         return None
-    ent = d.get("workloads", {}).get(f"{cfg}:{label}")
-    return ent
+    ent = d.get("workloads", {}).get(f"{cfg}:step")
+    if not ent:
+        return None
+    per = ent.get("per_kernel", {})
+    names = ["c4_kernel", "c4_hub_kernel"] if kernel == "c4_kernel" else [kernel]
+    hit = [per[n] for n in names if n in per]
+    if not hit:
+        return None
+    l2b = sum(p["l2_bytes"] for p in hit)
+    return {"dram_bytes": sum(p["dram_bytes"] for p in hit),
+            "l2_hit_pct": (sum((p["l2_hit_pct"] or 0) * p["l2_bytes"] for p in hit) / l2b) if l2b else None,
+            "launches": sum(p["launches"] for p in hit), "source": ent.get("source")}
 
 
 # kernels one full count launches: the generic executor runs count_kernel (+
@@ -298,6 +310,18 @@ FOLDED_LAUNCHES = {1: 3, 2: 1, 3: 2, 4: 2, 5: 3, 6: 2, 7: 4, 8: 3, 9: 3}
 # configs whose E (intersected elements) the generic executor's
 # metering pass measures in seconds; the others report count time only
 METERED_CONFIGS = ("cfg1", "cfg2")
+
+
+def launches_per_step(cfg, plans):
+    """Kernel launches of one step: counted by ncu for this config's step when
+    the committed summary has it (profiles/ncu_summary.json), else the sum of
+    the per-count figures above."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            per = json.load(f)["workloads"][f"{cfg}:step"]["per_kernel"]
+        return sum(int(p["launches"]) for p in per.values())
+    except Exception:
+        return sum(kernels_per_count(p)[0] for _, p in plans)
 
 
 def kernels_per_count(plan):
@@ -389,6 +413,7 @@ def our_arm(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     kern_ms = {label: [] for label, _ in plans}
+    phase_ms = [[], [], [], []]  # per timed step: count_kernel (K4), c4 pass, edge pass, vertex pass
     for _ in range(args.warmup):
         step(h)
         flush.add_(1)
@@ -405,6 +430,10 @@ def our_arm(args):
             for i, (label, _) in enumerate(plans):
                 kern_ms[label].append(res[i].kernel_ms)
             ev[s][1].record(stream)
+            ph = (ctypes.c_double * 4)()
+            N.check_gpu(lib.smg_phase_times(h, 0, ph))
+            for q in range(4):
+                phase_ms[q].append(ph[q])
             step_counts.append(cs)
         torch.cuda.synchronize(dev)
     barrier()
@@ -441,19 +470,27 @@ def our_arm(args):
     t_e2e = allmax(t_e2e) / e2e_steps
     e2e_value = E_total / t_e2e if metered else t_e2e
 
-    # ---- roofline of the dominant count (rank 0's shard) ---------------------
-    # Physical: DRAM bytes per count of the dominant pattern (count_kernel +
-    # heavy_kernel, one ncu --set full capture of this workload, committed in
-    # profiles/) / this run's live kernel time for that count / measured HBM
-    # peak.  Algorithmic: 4 B x E (a merge engine's element reads)
-    # / the same time -- reported separately, it is not a roofline.
-    dom = max(kern_ms, key=lambda k: statistics.mean(kern_ms[k]))
-    dom_ms = statistics.mean(kern_ms[dom])
-    alg_gbs = 4.0 * E[dom] / (dom_ms / 1e3) / 1e9 if metered and world == 1 else None
+    # ---- roofline of the dominant kernel (rank 0's shard) --------------------
+    # Physical: the kernel's DRAM bytes per step (dram__bytes_read + write of one
+    # ncu capture of this step, committed under profiles/) / its live device
+    # time per step (CUDA events on the launching stream, smg_phase_times or
+    # the count's kernel_ms) / the measured HBM peak.  Algorithmic: 4 B x E
+    # (the bytes a merge engine would stream) / the step's kernel
+    # time -- reported separately, it is not a roofline of this engine.
+    step_kernel_ms = sum(statistics.mean(v) for v in kern_ms.values())
+    alg_gbs = 4.0 * E_total / (step_kernel_ms / 1e3) / 1e9 if metered and world == 1 else None
     peak, peak_kind = load_peaks()
+    phase_names = ["count_kernel", "c4_kernel", "m4_edge_kernel", "m4_vertex_kernel"]
+    if any(statistics.mean(v) > 0 for v in phase_ms):
+        kernel_ms = {nm: statistics.mean(v) for nm, v in zip(phase_names, phase_ms)}
+    else:  # no closed-form batch in this config: one kernel_ms per count
+        kernel_ms = {f"{lbl} (all kernels of the count)": statistics.mean(v) for lbl, v in kern_ms.items()}
+    dom = max(kernel_ms, key=kernel_ms.get)
+    dom_ms = kernel_ms[dom]
     prof = load_profile(CONFIG, dom)
-    traffic = prof.get("dram_bytes_per_launch") if prof else None
+    traffic = prof.get("dram_bytes") if prof else None
     achieved = traffic / (dom_ms / 1e3) / 1e9 if traffic else None
+    frac = (achieved / peak) if achieved else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -486,9 +523,9 @@ def our_arm(args):
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": (f"folded kind {folded[dom]} (tindex.cu), one count of {dom}" if folded[dom]
-                                    else f"count_kernel + heavy_kernel, one count of {dom}"),
+                         "frac": frac, "traffic": traffic,
+                         "kernel": dom, "kernel_ms_per_step": dom_ms, "kernel_ms_all": kernel_ms,
+                         "kernel_launches_per_step": prof.get("launches") if prof else None,
                          "l2_hit_pct": prof.get("l2_hit_pct") if prof else None,
                          "peak_source": peak_kind,
                          "traffic_source": prof.get("source") if prof else None,
@@ -497,7 +534,7 @@ def our_arm(args):
                                          "note": "4 B x E / kernel time (E = elements a merge-based level "
                                                  "build consumes); hoisting, probe-side choice and leaf "
                                                  "batching read far fewer bytes, so this exceeds HBM"}},
-            "gpu_launches": args.steps * sum(kernels_per_count(p)[0] for _, p in plans),
+            "gpu_launches": args.steps * launches_per_step(CONFIG, plans),
             "clocks": clocks.summary(),
         }
         if cpu:

@@ -176,6 +176,14 @@ int smg_count_many_shard(const smg_graph* g, const smg_plan* plans, uint32_t num
                          uint32_t shard, uint32_t num_shards, uint32_t flags, smg_result* out);
 
 /*
+ * Device times (CUDA events on the launching stream, ms) of the kernels of the
+ * last closed-form 4-vertex count on a replica: ms[0] the 4-clique
+ * count_kernel, ms[1] the 4-cycle pass (c4_kernel + hub launches), ms[2]
+ * m4_edge_kernel, ms[3] m4_vertex_kernel.  For measurement (bench.py's roofline).
+ */
+int smg_phase_times(const smg_graph* g, int replica, double* ms);
+
+/*
  * One shard of the level-1 units on replica `replica` of g (one process per
  * GPU: shard = rank, num_shards = world size).  Shards of any num_shards
  * partition the units exactly, so the sum over shards equals smg_count.

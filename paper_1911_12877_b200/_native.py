@@ -115,6 +115,7 @@ def gpu_lib():
             _bind(lib, "smg_count_many", ctypes.c_int,
                   [_P, ctypes.POINTER(SmgPlan), ctypes.c_uint32, ctypes.c_uint, ctypes.c_uint32,
                    ctypes.POINTER(SmgResult)])
+            _bind(lib, "smg_phase_times", ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_double)])
             _bind(lib, "smg_count_many_shard", ctypes.c_int,
                   [_P, ctypes.POINTER(SmgPlan), ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
                    ctypes.c_uint32, ctypes.POINTER(SmgResult)])

@@ -2302,6 +2302,8 @@ struct Replica {
   cudaStream_t user_stream = nullptr;  // set by smg_graph_set_stream (not owned)
   cudaStream_t active() const { return user_stream ? user_stream : stream; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // created on first use (m4_count)
+  double phase_ms[4] = {0, 0, 0, 0};  // last m4_count: 4-clique count, C4 pass, edge pass, vertex pass
   // cost-balanced shard map, cached per (num_shards, unit_bound)
   uint32_t map_shards = 0;
   int map_unit_bound = -1;
@@ -2834,6 +2836,14 @@ const int g_relabel = [] {
   return (e && *e == '0') ? 0 : 1;
 }();
 
+// SMG_M4_HUB_DEGREE: degree from which a centre of the 4-cycle pass is scattered
+// by the whole grid (tests lower it so small graphs take the hub path).
+const uint32_t g_m4_hub = [] {
+  const char* e = std::getenv("SMG_M4_HUB_DEGREE");
+  const long v = e ? std::atol(e) : 0;
+  return v > 0 ? static_cast<uint32_t>(v) : kM4HubDegree;
+}();
+
 bool clique_plan(const smg_plan& p) {
   if (p.depth < 3) return false;
   for (uint32_t i = 1; i < p.depth; ++i)
@@ -3002,6 +3012,14 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   a.num_shards = L.num_shards;
   a.shard = L.shard;
   a.units_per_edge = 1;
+  if ((need & (1u << kM4C4)) && g.max_degree >= g_m4_hub) {
+    // degrees descend with the id on the ordered copy: the hubs are a prefix
+    const uint64_t k = std::min<uint64_t>(g.n, kM4MaxHubs);
+    std::vector<unsigned long long> ho(k + 1);
+    SMG_CUDA(cudaMemcpyAsync(ho.data(), r.off, (k + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SMG_CUDA(cudaStreamSynchronize(st));
+    while (a.hub_count < k && ho[a.hub_count + 1] - ho[a.hub_count] >= g_m4_hub) ++a.hub_count;
+  }
   a.dmax = g.max_degree;
   a.dense = r.fast_dense;
   a.part = r.part_dev;
@@ -3012,7 +3030,10 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   a.overflow = &r.ctr->overflow;
   SMG_CUDA(cudaMemsetAsync(r.ctr, 0, sizeof(Counters), st));
   SMG_CUDA(cudaEventRecord(r.ev0, st));
-  if (g.slots && m4_launch(a, need, blocks, st)) return fail(SMG_EIO, "4-vertex closed-form kernel launch failed");
+  for (cudaEvent_t& e : r.phase_ev)
+    if (!e) SMG_CUDA(cudaEventCreate(&e));
+  if (g.slots && m4_launch(a, need, blocks, st, r.phase_ev))
+    return fail(SMG_EIO, "4-vertex closed-form kernel launch failed");
   SMG_CUDA(cudaGetLastError());
   SMG_CUDA(cudaEventRecord(r.ev1, st));
   SMG_CUDA(cudaMemcpyAsync(r.part_host, r.part_dev, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -3020,6 +3041,12 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   SMG_CUDA(cudaStreamSynchronize(st));
   float t = 0.f;
   SMG_CUDA(cudaEventElapsedTime(&t, r.ev0, r.ev1));
+  r.phase_ms[0] = k4_ms;
+  for (int q = 0; q < 3; ++q) {
+    float pt = 0.f;
+    if (g.slots) SMG_CUDA(cudaEventElapsedTime(&pt, r.phase_ev[q], r.phase_ev[q + 1]));
+    r.phase_ms[q + 1] = pt;
+  }
   __int128 S[kM4Regions];
   for (int q = 0; q < kM4Regions; ++q) {
     S[q] = 0;
@@ -3218,6 +3245,8 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->host_ctr) cudaFreeHost(r->host_ctr);
     if (r->ev0) cudaEventDestroy(r->ev0);
     if (r->ev1) cudaEventDestroy(r->ev1);
+    for (cudaEvent_t e : r->phase_ev)
+      if (e) cudaEventDestroy(e);
     if (r->stream) cudaStreamDestroy(r->stream);
     delete r;
   }
@@ -3457,6 +3486,15 @@ int smg_graph_set_stream(smg_graph* g, int replica, void* stream) {
   Replica& r = *g->reps[replica];
   std::lock_guard<std::mutex> lock(r.mu);
   r.user_stream = static_cast<cudaStream_t>(stream);
+  return SMG_OK;
+}
+
+int smg_phase_times(const smg_graph* g, int replica, double* ms) {
+  if (!g || !ms) return fail(SMG_EINPUT, "null argument");
+  if (replica < 0 || replica >= static_cast<int>(g->reps.size())) return fail(SMG_EINPUT, "bad replica");
+  Replica& r = *g->reps[replica];
+  std::lock_guard<std::mutex> lock(r.mu);
+  for (int q = 0; q < 4; ++q) ms[q] = r.phase_ms[q];
   return SMG_OK;
 }
 

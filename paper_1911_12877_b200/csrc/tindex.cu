@@ -1069,8 +1069,8 @@ __device__ __forceinline__ i128 warp_sum128(i128 v) {
 
 // every thread calls it once, at the end; sums the block and stores its share
 __device__ void store_partial(const FastArgs& a, i128 v, ull units) {
-  __shared__ i128 red[kFastThreads / 32];
-  __shared__ ull ured[kFastThreads / 32];
+  __shared__ i128 red[32];  // up to 1024 threads per CTA
+  __shared__ ull ured[32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   __syncthreads();  // a kernel may call it once per sum: the previous read of red[] is over
   v = warp_sum128(v);
@@ -1596,13 +1596,48 @@ __device__ __forceinline__ bool owns_vertex(const FastArgs& a, uint32_t v) {
 // C4: one CTA per centre c, dense per-CTA table w_c (n words, kept zero between
 // centres).  Each touch adds atomicAdd's return value: the k-th increment of a
 // word returns k - 1, and 0 + 1 + ... + (w - 1) = C(w, 2).
-__global__ void __launch_bounds__(kFastThreads) c4_kernel(const FastArgs a) {
+// One list of the scatter: x in N(u), x > c (c itself is in N(u): the suffix
+// starts right after it).  Four touches in flight per lane.
+constexpr int kC4Threads = 1024;
+constexpr int kM4EdgeThreads = 512;
+
+template <bool RESET>
+__device__ __forceinline__ ull c4_list(const FastArgs& a, uint32_t* cnt, uint32_t c, uint32_t u, int lane) {
+  const ull uo = a.off[u];
+  const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
+  const uint32_t x0 = lb32(a.adj + uo, du, c + 1u);
+  const uint32_t* X = a.adj + uo;
+  ull s = 0;
+  uint32_t k = x0 + lane;
+  for (; k + 96 < du; k += 128) {
+    const uint32_t xa = X[k], xb = X[k + 32], xc = X[k + 64], xd = X[k + 96];
+    if (RESET) {
+      cnt[xa] = 0u;
+      cnt[xb] = 0u;
+      cnt[xc] = 0u;
+      cnt[xd] = 0u;
+    } else {
+      const uint32_t ra = atomicAdd(&cnt[xa], 1u), rb = atomicAdd(&cnt[xb], 1u);
+      const uint32_t rc = atomicAdd(&cnt[xc], 1u), rd = atomicAdd(&cnt[xd], 1u);
+      s += static_cast<ull>(ra) + rb + rc + rd;
+    }
+  }
+  for (; k < du; k += 32) {
+    if (RESET) cnt[X[k]] = 0u;
+    else s += atomicAdd(&cnt[X[k]], 1u);
+  }
+  return s;
+}
+
+// kC4Threads per CTA (the tables allow two CTAs per SM: 32 warps each fill it).
+__global__ void __launch_bounds__(kC4Threads) c4_kernel(const FastArgs a) {
   __shared__ ull center_sh;
+  __shared__ i128 red[kC4Threads / 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint32_t* cnt = a.dense + static_cast<uint64_t>(blockIdx.x) * a.n;
   i128 acc = 0;
   for (;;) {
-    const ull c = next_center(a, &center_sh);
+    const ull c = a.hub_count + next_center(a, &center_sh);  // centres below hub_count: c4_hub_kernel
     if (c >= a.n) break;
     if (!owns_vertex(a, static_cast<uint32_t>(c))) continue;
     const ull co = a.off[c];
@@ -1612,31 +1647,55 @@ __global__ void __launch_bounds__(kFastThreads) c4_kernel(const FastArgs a) {
     if (np < 2) continue;
     const uint32_t* U = a.adj + co + k0;
     ull s = 0;
-    for (uint32_t j = wib; j < np; j += nw) {
-      const uint32_t u = U[j];
-      const ull uo = a.off[u];
-      const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
-      // x in N(u), x > c (c itself is in N(u): the suffix starts right after it)
-      const uint32_t x0 = lb32(a.adj + uo, du, static_cast<uint32_t>(c) + 1u);
-      for (uint32_t k = x0 + lane; k < du; k += 32) s += atomicAdd(&cnt[a.adj[uo + k]], 1u);
-    }
+    for (uint32_t j = wib; j < np; j += nw) s += c4_list<false>(a, cnt, static_cast<uint32_t>(c), U[j], lane);
     acc += static_cast<i128>(s);
     __syncthreads();
-    for (uint32_t j = wib; j < np; j += nw) {
-      const uint32_t u = U[j];
-      const ull uo = a.off[u];
-      const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
-      const uint32_t x0 = lb32(a.adj + uo, du, static_cast<uint32_t>(c) + 1u);
-      for (uint32_t k = x0 + lane; k < du; k += 32) cnt[a.adj[uo + k]] = 0u;
-    }
+    for (uint32_t j = wib; j < np; j += nw) c4_list<true>(a, cnt, static_cast<uint32_t>(c), U[j], lane);
   }
-  store_partial(a, acc, 0);
+  acc = warp_sum128(acc);
+  if (lane == 0) red[wib] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = 0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    a.part[2 * blockIdx.x] = static_cast<ull>(t);
+    a.part[2 * blockIdx.x + 1] = static_cast<ull>(t >> 64);
+  }
+}
+
+// A hub centre (the first a.hub_count ids of the degree-ordered CSR): the
+// whole grid scatters it into table 0, one launch for the scatter (the CTA's
+// sum is added to its partial) and one for the reset, so the largest centres
+// do not serialise on one CTA at the tail.
+template <bool RESET>
+__global__ void __launch_bounds__(kFastThreads) c4_hub_kernel(const FastArgs a, uint32_t c) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, tw = (gridDim.x * blockDim.x) >> 5;
+  const ull co = a.off[c];
+  const uint32_t dc = static_cast<uint32_t>(a.off[c + 1] - co);
+  const uint32_t k0 = lb32(a.adj + co, dc, c + 1u);
+  const uint32_t np = dc - k0;
+  const uint32_t* U = a.adj + co + k0;
+  ull s = 0;
+  for (uint32_t j = gw; j < np; j += tw) s += c4_list<RESET>(a, a.dense, c, U[j], lane);
+  if (RESET) return;
+  __shared__ ull red[kFastThreads / 32];
+  s = warp_sum(s);
+  if (lane == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = static_cast<i128>((static_cast<unsigned __int128>(a.part[2 * blockIdx.x + 1]) << 64) |
+                               a.part[2 * blockIdx.x]);
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += static_cast<i128>(red[w]);
+    a.part[2 * blockIdx.x] = static_cast<ull>(t);
+    a.part[2 * blockIdx.x + 1] = static_cast<ull>(t >> 64);
+  }
 }
 
 // Per undirected edge (slot e = (u, v), u < v; the shard that owns u):
 // C(t, 2), t and (d_u - 1)(d_v - 1); and tv[x] += t at the owned endpoints
 // (tv[x] = 2 t_x once every edge at x is in; only when a.acc0 is given).
-__global__ void __launch_bounds__(kFastThreads) m4_edge_kernel(const FastArgs a) {
+__global__ void __launch_bounds__(kM4EdgeThreads, 2) m4_edge_kernel(const FastArgs a) {
   const int lane = threadIdx.x & 31;
   i128 acc_d = 0, acc_t3 = 0, acc_p4 = 0;
   ull units = 0;
@@ -1733,23 +1792,34 @@ __global__ void __launch_bounds__(kFastThreads) m4_vertex_kernel(const FastArgs 
 }
 
 // need: bit r set = region r (kM4*) is wanted.  a.part: kM4Regions x blocks pairs.
-int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st) {
+// ev (may be null): 4 events recorded before the C4 pass, after it, after the
+// edge pass and after the vertex pass (per-kernel device times).
+int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st, cudaEvent_t* ev) {
   if (cudaMemsetAsync(a.part, 0, 2 * kM4Regions * blocks * sizeof(ull), st) != cudaSuccess) return 1;
+  if (ev) cudaEventRecord(ev[0], st);
   if (need & (1u << kM4C4)) {
     if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
     FastArgs w = a;
     w.part = a.part + 2 * blocks * kM4C4;
-    c4_kernel<<<blocks, kFastThreads, 0, st>>>(w);
+    c4_kernel<<<blocks, kC4Threads, 0, st>>>(w);  // stores its partials; the hub launches add to them
+    for (uint32_t c = 0; c < a.hub_count; ++c) {
+      if (a.num_shards > 1 && c % a.num_shards != a.shard) continue;
+      c4_hub_kernel<false><<<blocks, kFastThreads, 0, st>>>(w, c);
+      c4_hub_kernel<true><<<blocks, kFastThreads, 0, st>>>(w, c);
+    }
     if (cudaGetLastError() != cudaSuccess) return 1;
   }
+  if (ev) cudaEventRecord(ev[1], st);
   FastArgs w = a;
   if (!(need & (1u << kM4Paw))) w.acc0 = nullptr;  // no per-vertex triangle counts needed
-  m4_edge_kernel<<<blocks, kFastThreads, 0, st>>>(w);
+  m4_edge_kernel<<<blocks, kM4EdgeThreads, 0, st>>>(w);
   if (cudaGetLastError() != cudaSuccess) return 1;
+  if (ev) cudaEventRecord(ev[2], st);
   if (need & ((1u << kM4Paw) | (1u << kM4Star))) {
     m4_vertex_kernel<<<blocks, kFastThreads, 0, st>>>(w);
     if (cudaGetLastError() != cudaSuccess) return 1;
   }
+  if (ev) cudaEventRecord(ev[3], st);
   return 0;
 }
 

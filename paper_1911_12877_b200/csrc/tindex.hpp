@@ -54,6 +54,7 @@ struct FastArgs {
   uint32_t num_shards;                 // > 1: shard map below
   uint32_t shard;                      // this shard (m4_launch: vertices dealt round-robin)
   uint32_t units_per_edge;             // m4_launch: level-1 units per undirected edge (1: v1 < v0, else 2)
+  uint32_t hub_count;                  // m4_launch: centres [0, hub_count) take the grid-wide C4 path
   const unsigned long long* map_begin;
   const unsigned long long* map_pref;
   uint32_t map_k;
@@ -109,7 +110,9 @@ struct M4Weights {
   }
 };
 bool m4_weights(int kind, M4Weights* w);
-int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st);
+constexpr uint32_t kM4HubDegree = 16384;  // centres of at least this degree are scattered by the whole grid
+constexpr uint32_t kM4MaxHubs = 16384;
+int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st, cudaEvent_t* ev);
 // Sum over index entries of k4 * (k4 - 1) (every entry of the index; needs
 // the k4 array).  Synchronous.
 int tindex_k4_pairs(const TIndex& t, int num_sms, cudaStream_t st, unsigned long long* out, std::string* err);

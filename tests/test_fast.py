@@ -154,3 +154,30 @@ def test_count_many_shares_work_and_matches_single_counts(spec, port):
         N.check_gpu(N.gpu_lib().smg_count_many_shard(g.device_handle((0,)), sm, len(plans), 0, i, 3, 0, res))
         tot = [t + (int(res[k].count_hi) << 64) + int(res[k].count) for k, t in enumerate(tot)]
     assert tot == [r.count for r in many]
+
+
+@pytest.mark.gpu
+def test_four_cycle_hub_path_in_subprocess():
+    """The grid-wide scatter of hub centres (c4_hub_kernel) only engages from
+    degree 16384; SMG_M4_HUB_DEGREE=6 (read when the library loads) sends most
+    centres of a small graph through it.  Totals and 3-shard sums must equal the
+    generic executor's."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys
+sys.path.insert(0, %r)
+from paper_1911_12877_b200 import configs, count_result, count_shard, named_plan
+from paper_1911_12877_b200.plan import motif_plans
+g = configs.load(configs.GraphSpec("rmat", (12, 8, 0.57, 0.19, 0.19), 11))
+plans = [named_plan("rectangle")] + [r["plan"] for r in motif_plans(4)]
+for p in plans:
+    want = count_result(g, p, generic=True).count
+    assert count_result(g, p).count == want
+    assert sum(count_shard(g, p, i, 3).count for i in range(3)) == want
+print("hub path OK")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SMG_M4_HUB_DEGREE="6"),
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0 and "hub path OK" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]

@@ -1,5 +1,6 @@
-"""Small single-pattern run for ncu: python tools/ncu_target.py <spec|cfgN> <pattern> [reps]
-spec: rmat:SCALE:EF  (seeded like the configs).  First call warms up."""
+"""Small single-pattern run for ncu: python tools/ncu_target.py <spec|cfgN> <pattern|step> [reps]
+spec: rmat:SCALE:EF  (seeded like the configs).  First call warms up.  "step" =
+every pattern of the config in one smg_count_many call (bench.py's step)."""
 import os
 import sys
 
@@ -17,7 +18,10 @@ else:
 plans = dict(configs.config_patterns("cfg2"))
 plans.update(dict(configs.config_patterns("cfg3")))
 plans.update({"triangle": smg.named_plan("triangle")})
-plan = plans[pat]
 for i in range(reps + 1):
-    r = smg.count_result(g, plan)
+    if pat == "step":
+        res = smg.count_many(g, [p for _, p in configs.config_patterns(spec)])
+        print(f"{spec} step: counts={[r.count for r in res]} kernel={sum(r.kernel_ms for r in res):.2f} ms", flush=True)
+        continue
+    r = smg.count_result(g, plans[pat])
     print(f"{spec} {pat}: count={r.count} kernel={r.kernel_ms:.2f} ms", flush=True)
