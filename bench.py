@@ -279,7 +279,7 @@ def load_profile(cfg, kernel):
     """ncu figures (DRAM bytes per step, L2 hit rate) of one kernel of this
     config's step, from the committed summary (profiles/ncu_summary.json,
     written by tools/traffic_summary.py).  The c4 phase sums c4_kernel and the
-    c4_hub_kernel launches."""
+    c4_hub_kernel / c4_group_kernel launches."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
@@ -289,7 +289,7 @@ def load_profile(cfg, kernel):
     if not ent:
         return None
     per = ent.get("per_kernel", {})
-    names = ["c4_kernel", "c4_hub_kernel"] if kernel == "c4_kernel" else [kernel]
+    names = ["c4_kernel", "c4_hub_kernel", "c4_group_kernel"] if kernel == "c4_kernel" else [kernel]
     hit = [per[n] for n in names if n in per]
     if not hit:
         return None
@@ -453,6 +453,7 @@ def our_arm(args):
     d2h = 48 * len(plans)
     e2e_steps = max(1, min(args.steps, 3))
     t_e2e = 0.0
+    e2e_parts = {"graph_create_ms": 0.0, "count_ms": 0.0, "graph_destroy_ms": 0.0}
     for s in range(e2e_steps + 1):
         barrier()
         t0 = time.perf_counter()
@@ -461,12 +462,16 @@ def our_arm(args):
         N.check_gpu(lib.smg_graph_create(ctypes.cast(off_pin.data_ptr(), ctypes.POINTER(ctypes.c_uint64)),
                                          ctypes.cast(adj_pin.data_ptr(), ctypes.POINTER(ctypes.c_uint32)),
                                          graph.n, dev_arr, 1, ctypes.byref(gh)))
+        t1 = time.perf_counter()
         res = step(gh)
         cs = [int(res[i].count) for i in range(len(plans))]
+        t2 = time.perf_counter()
         lib.smg_graph_destroy(gh)
-        dt = time.perf_counter() - t0
+        t3 = time.perf_counter()
         if s > 0:  # first iteration warms the allocator / context
-            t_e2e += dt
+            t_e2e += t3 - t0
+            for k, v in zip(e2e_parts, (t1 - t0, t2 - t1, t3 - t2)):
+                e2e_parts[k] += 1e3 * v / e2e_steps
     t_e2e = allmax(t_e2e) / e2e_steps
     e2e_value = E_total / t_e2e if metered else t_e2e
 
@@ -521,7 +526,7 @@ def our_arm(args):
                        "parallelism": f"units sharded over {world} GPU(s), 1 allreduce",
                        "l2": "flushed between timed steps (512 MB write)"},
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3, **e2e_parts},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": frac, "traffic": traffic,
                          "kernel": dom, "kernel_ms_per_step": dom_ms, "kernel_ms_all": kernel_ms,

@@ -2329,6 +2329,11 @@ struct Replica {
   // degree-ordered copy of the CSR (orient_reindex ids: 0 = highest degree),
   // built on first use for the label-free full counts (cliques, 4-cycles)
   DevCSR ocsr;
+  bool tiers_valid = false;                            // hub / group tier bounds of the ordered copy
+  uint32_t hub_count = 0, group_end = 0;
+  uint32_t* gtab = nullptr;                            // group-tier tables of the 4-cycle pass
+  size_t gtab_bytes = 0;
+  unsigned long long* gbar = nullptr;
   bool view_oriented = false;                          // off/adj/src currently point at ocsr
   bool map_oriented = false;                           // labelling the cached shard map belongs to
   std::mutex mu;
@@ -2363,6 +2368,16 @@ struct WorkSet {
   size_t warp_bitmaps_bytes = 0;
   uint32_t* heavy_rows = nullptr;
   size_t heavy_rows_bytes = 0;
+  // closed-form 4-vertex counts (m4_count): dense per-CTA tables and group
+  // tables (both kept zero by the kernels), barrier counters, partial sums
+  uint32_t* fast_dense = nullptr;
+  size_t fast_dense_bytes = 0;
+  uint32_t* gtab = nullptr;
+  size_t gtab_bytes = 0;
+  unsigned long long* gbar = nullptr;
+  unsigned long long* part_dev = nullptr;
+  unsigned long long* part_host = nullptr;
+  size_t part_words = 0;
 };
 std::mutex g_pool_mu;
 WorkSet g_pool[64];  // one parked set per device ordinal
@@ -2375,6 +2390,11 @@ void free_work(WorkSet& w) {
   if (w.local_rows) cudaFree(w.local_rows);
   if (w.warp_bitmaps) cudaFree(w.warp_bitmaps);
   if (w.heavy_rows) cudaFree(w.heavy_rows);
+  if (w.fast_dense) cudaFree(w.fast_dense);
+  if (w.gtab) cudaFree(w.gtab);
+  if (w.gbar) cudaFree(w.gbar);
+  if (w.part_dev) cudaFree(w.part_dev);
+  if (w.part_host) cudaFreeHost(w.part_host);
   w = WorkSet();
 }
 
@@ -2391,6 +2411,20 @@ void park_work(Replica& r) {
   w.warp_bitmaps_bytes = r.warp_bitmaps_bytes;
   w.heavy_rows = r.heavy_rows;
   w.heavy_rows_bytes = r.heavy_rows_bytes;
+  w.fast_dense = r.fast_dense;
+  w.fast_dense_bytes = r.fast_dense_bytes;
+  w.gtab = r.gtab;
+  w.gtab_bytes = r.gtab_bytes;
+  w.gbar = r.gbar;
+  w.part_dev = r.part_dev;
+  w.part_host = r.part_host;
+  w.part_words = r.part_words;
+  r.fast_dense = nullptr;
+  r.gtab = nullptr;
+  r.gbar = nullptr;
+  r.part_dev = nullptr;
+  r.part_host = nullptr;
+  r.fast_dense_bytes = r.gtab_bytes = r.part_words = 0;
   if (r.device < 0 || r.device >= 64) {
     free_work(w);
     return;
@@ -2417,6 +2451,14 @@ void adopt_work(Replica& r) {
   r.warp_bitmaps_bytes = w.warp_bitmaps_bytes;
   r.heavy_rows = w.heavy_rows;
   r.heavy_rows_bytes = w.heavy_rows_bytes;
+  r.fast_dense = w.fast_dense;
+  r.fast_dense_bytes = w.fast_dense_bytes;
+  r.gtab = w.gtab;
+  r.gtab_bytes = w.gtab_bytes;
+  r.gbar = w.gbar;
+  r.part_dev = w.part_dev;
+  r.part_host = w.part_host;
+  r.part_words = w.part_words;
   w = WorkSet();
   g_pool_used[r.device] = false;
 }
@@ -2841,8 +2883,28 @@ const int g_relabel = [] {
 const uint32_t g_m4_hub = [] {
   const char* e = std::getenv("SMG_M4_HUB_DEGREE");
   const long v = e ? std::atol(e) : 0;
-  return v > 0 ? static_cast<uint32_t>(v) : kM4HubDegree;
+  return v > 0 ? static_cast<uint32_t>(std::min<long>(v, 32768)) : kM4HubDegree;  // group tables hold 16-bit counts
 }();
+// SMG_M4_GROUP_DEGREE: degree from which a centre takes the group tier (0 = off).
+const uint32_t g_m4_group = [] {
+  const char* e = std::getenv("SMG_M4_GROUP_DEGREE");
+  return e ? static_cast<uint32_t>(std::max<long>(0, std::atol(e))) : kM4GroupDegree;
+}();
+
+// First vertex of the degree-ordered CSR (degrees descend with the id) whose
+// degree is below `threshold`: a binary search over device offsets.
+int first_below(const unsigned long long* off, uint64_t n, uint64_t threshold, uint32_t* out) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    unsigned long long o[2];
+    SMG_CUDA(cudaMemcpy(o, off + mid, sizeof(o), cudaMemcpyDeviceToHost));
+    if (o[1] - o[0] >= threshold) lo = mid + 1;
+    else hi = mid;
+  }
+  *out = static_cast<uint32_t>(lo);
+  return SMG_OK;
+}
 
 bool clique_plan(const smg_plan& p) {
   if (p.depth < 3) return false;
@@ -2965,16 +3027,27 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   }
   cudaStream_t st = r.active();
   const unsigned blocks = static_cast<unsigned>(r.num_sms) * 2;
-  const size_t dense_need = (need & (1u << kM4C4))
-                                ? static_cast<size_t>(blocks) * std::max<uint64_t>(g.n, 1) * sizeof(uint32_t)
-                                : 0;
-  if (dense_need > r.fast_dense_bytes) {
-    if (r.fast_dense) cudaFree(r.fast_dense);
-    r.fast_dense = nullptr;
-    r.fast_dense_bytes = 0;
-    SMG_CUDA(cudaMalloc(&r.fast_dense, dense_need));
-    SMG_CUDA(cudaMemsetAsync(r.fast_dense, 0, dense_need, st));
-    r.fast_dense_bytes = dense_need;
+  // one dense table (n words) per CTA of c4_kernel: as many as fit in half of
+  // the free memory (a graph near the 2^32-vertex limit still gets one)
+  unsigned c4_blocks = blocks;
+  if (need & (1u << kM4C4)) {
+    const size_t table = std::max<uint64_t>(g.n, 1) * sizeof(uint32_t);
+    if (static_cast<size_t>(blocks) * table > r.fast_dense_bytes) {
+      size_t free_b = 0, total_b = 0;
+      SMG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      free_b += r.fast_dense_bytes;  // the current buffer is released first
+      c4_blocks = static_cast<unsigned>(std::min<size_t>(blocks, std::max<size_t>(1, free_b / 2 / table)));
+      if (static_cast<size_t>(c4_blocks) * table > r.fast_dense_bytes) {
+        if (r.fast_dense) cudaFree(r.fast_dense);
+        r.fast_dense = nullptr;
+        r.fast_dense_bytes = 0;
+        SMG_CUDA(cudaMalloc(&r.fast_dense, static_cast<size_t>(c4_blocks) * table));
+        SMG_CUDA(cudaMemsetAsync(r.fast_dense, 0, static_cast<size_t>(c4_blocks) * table, st));
+        r.fast_dense_bytes = static_cast<size_t>(c4_blocks) * table;
+      } else {
+        c4_blocks = static_cast<unsigned>(r.fast_dense_bytes / table);
+      }
+    }
   }
   const size_t words = 2 * static_cast<size_t>(kM4Regions) * blocks;
   if (words > r.part_words) {
@@ -3012,13 +3085,44 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   a.num_shards = L.num_shards;
   a.shard = L.shard;
   a.units_per_edge = 1;
-  if ((need & (1u << kM4C4)) && g.max_degree >= g_m4_hub) {
-    // degrees descend with the id on the ordered copy: the hubs are a prefix
-    const uint64_t k = std::min<uint64_t>(g.n, kM4MaxHubs);
-    std::vector<unsigned long long> ho(k + 1);
-    SMG_CUDA(cudaMemcpyAsync(ho.data(), r.off, (k + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    SMG_CUDA(cudaStreamSynchronize(st));
-    while (a.hub_count < k && ho[a.hub_count + 1] - ho[a.hub_count] >= g_m4_hub) ++a.hub_count;
+  a.c4_blocks = c4_blocks;
+  if (need & (1u << kM4C4)) {
+    if (!r.tiers_valid) {
+      SMG_CUDA(cudaStreamSynchronize(st));
+      int trc = first_below(r.off, g.n, g_m4_hub, &r.hub_count);
+      if (trc) return trc;
+      r.group_end = r.hub_count;
+      if (r.hub_count > kM4MaxHubs) {
+        // more hubs than the launch loop takes: the rest go one CTA each (32-bit
+        // tables); no group tier, its 16-bit counters assume degrees below the hub degree
+        r.hub_count = r.group_end = kM4MaxHubs;
+      } else if (g_m4_group && g_m4_group < g_m4_hub) {
+        trc = first_below(r.off, g.n, g_m4_group, &r.group_end);
+        if (trc) return trc;
+        r.group_end = std::max(r.group_end, r.hub_count);
+      }
+      r.tiers_valid = true;
+    }
+    a.hub_count = r.hub_count;
+    a.group_end = r.group_end;
+    if (a.group_end > a.hub_count) {
+      // as many group tables as stay L2-resident together (about 64 MB), at most 16
+      const size_t table = ((g.n + 1) / 2) * sizeof(uint32_t);
+      const uint32_t groups = static_cast<uint32_t>(std::min<size_t>(16, std::max<size_t>(1, (64u << 20) / table)));
+      const size_t need_bytes = groups * table;
+      if (need_bytes > r.gtab_bytes) {
+        if (r.gtab) cudaFree(r.gtab);
+        r.gtab = nullptr;
+        r.gtab_bytes = 0;
+        SMG_CUDA(cudaMalloc(&r.gtab, need_bytes));
+        SMG_CUDA(cudaMemsetAsync(r.gtab, 0, need_bytes, st));
+        r.gtab_bytes = need_bytes;
+      }
+      if (!r.gbar) SMG_CUDA(cudaMalloc(&r.gbar, 16 * sizeof(unsigned long long)));
+      a.groups = groups;
+      a.gtab = r.gtab;
+      a.gbar = r.gbar;
+    }
   }
   a.dmax = g.max_degree;
   a.dense = r.fast_dense;
@@ -3237,6 +3341,8 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->fast_scratch) cudaFree(r->fast_scratch);
     if (r->fast_acc) cudaFree(r->fast_acc);
     if (r->fast_dense) cudaFree(r->fast_dense);
+    if (r->gtab) cudaFree(r->gtab);
+    if (r->gbar) cudaFree(r->gbar);
     if (r->ocsr.off) cudaFree(r->ocsr.off);
     if (r->ocsr.adj) cudaFree(r->ocsr.adj);
     if (r->ocsr.src) cudaFree(r->ocsr.src);

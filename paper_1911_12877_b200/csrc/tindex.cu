@@ -1637,7 +1637,7 @@ __global__ void __launch_bounds__(kC4Threads) c4_kernel(const FastArgs a) {
   uint32_t* cnt = a.dense + static_cast<uint64_t>(blockIdx.x) * a.n;
   i128 acc = 0;
   for (;;) {
-    const ull c = a.hub_count + next_center(a, &center_sh);  // centres below hub_count: c4_hub_kernel
+    const ull c = a.group_end + next_center(a, &center_sh);  // smaller ids: the hub and group tiers
     if (c >= a.n) break;
     if (!owns_vertex(a, static_cast<uint32_t>(c))) continue;
     const ull co = a.off[c];
@@ -1687,6 +1687,109 @@ __global__ void __launch_bounds__(kFastThreads) c4_hub_kernel(const FastArgs a, 
     i128 t = static_cast<i128>((static_cast<unsigned __int128>(a.part[2 * blockIdx.x + 1]) << 64) |
                                a.part[2 * blockIdx.x]);
     for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += static_cast<i128>(red[w]);
+    a.part[2 * blockIdx.x] = static_cast<ull>(t);
+    a.part[2 * blockIdx.x + 1] = static_cast<ull>(t >> 64);
+  }
+}
+
+// Group tier of the C4 pass: centres [hub_count, group_end) (degree from
+// kM4GroupDegree up to the hub degree) carry ~95% of the table touches.  The
+// grid splits into a.groups groups of CTAs; a group owns one table of 16-bit
+// counters packed in pairs (n / 2 words; counts stay below the hub degree), so
+// the a.groups tables together stay resident in the 126 MB L2 instead of
+// streaming 32-byte DRAM sectors per 4-byte touch.  Group g takes centres
+// hub_count + g, + groups, ... (degrees descend with the id: round-robin is
+// largest-first); its CTAs split the centre's lists and meet at a group
+// barrier after the scatter and after the reset.  Cooperative launch: every
+// CTA is resident, so the spin barrier cannot starve.
+__device__ __forceinline__ void group_barrier(ull* bar, ull& target, unsigned ctas) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += ctas;
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    while (*reinterpret_cast<volatile ull*>(bar) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <bool RESET>
+__device__ __forceinline__ ull c4_list16(const FastArgs& a, uint32_t* tab, uint32_t c, uint32_t u, int lane) {
+  const ull uo = a.off[u];
+  const uint32_t du = static_cast<uint32_t>(a.off[u + 1] - uo);
+  const uint32_t x0 = lb32(a.adj + uo, du, c + 1u);
+  const uint32_t* X = a.adj + uo;
+  ull s = 0;
+  uint32_t k = x0 + lane;
+  for (; k + 96 < du; k += 128) {
+    const uint32_t xa = X[k], xb = X[k + 32], xc = X[k + 64], xd = X[k + 96];
+    if (RESET) {
+      tab[xa >> 1] = 0u;  // both halves end the reset phase at zero
+      tab[xb >> 1] = 0u;
+      tab[xc >> 1] = 0u;
+      tab[xd >> 1] = 0u;
+    } else {
+      const uint32_t sa = (xa & 1u) << 4, sb = (xb & 1u) << 4, sc = (xc & 1u) << 4, sd = (xd & 1u) << 4;
+      const uint32_t ra = atomicAdd(&tab[xa >> 1], 1u << sa), rb = atomicAdd(&tab[xb >> 1], 1u << sb);
+      const uint32_t rc = atomicAdd(&tab[xc >> 1], 1u << sc), rd = atomicAdd(&tab[xd >> 1], 1u << sd);
+      s += static_cast<ull>((ra >> sa) & 0xffffu) + ((rb >> sb) & 0xffffu) + ((rc >> sc) & 0xffffu) +
+           ((rd >> sd) & 0xffffu);
+    }
+  }
+  for (; k < du; k += 32) {
+    const uint32_t x = X[k];
+    if (RESET) {
+      tab[x >> 1] = 0u;
+    } else {
+      const uint32_t sh = (x & 1u) << 4;
+      s += (atomicAdd(&tab[x >> 1], 1u << sh) >> sh) & 0xffffu;
+    }
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(kC4Threads, 2) c4_group_kernel(const FastArgs a) {
+  __shared__ ull red[kC4Threads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned cpg = gridDim.x / a.groups;  // the launch makes gridDim.x = groups x cpg
+  const unsigned g = blockIdx.x / cpg, rank = blockIdx.x % cpg;
+  const uint64_t words = (a.n + 1) / 2;
+  uint32_t* tab = a.gtab + static_cast<uint64_t>(g) * words;
+  ull* bar = a.gbar + g;
+  ull target = 0, s = 0;
+  for (uint64_t c64 = static_cast<uint64_t>(a.hub_count) + g; c64 < a.group_end; c64 += a.groups) {
+    const uint32_t c = static_cast<uint32_t>(c64);
+    if (!owns_vertex(a, c)) continue;
+    const ull co = a.off[c];
+    const uint32_t dc = static_cast<uint32_t>(a.off[c + 1] - co);
+    const uint32_t k0 = lb32(a.adj + co, dc, c + 1u);
+    const uint32_t np = dc - k0;
+    if (np < 2) continue;  // the same decision in every CTA of the group
+    const uint32_t* U = a.adj + co + k0;
+    for (uint32_t j = rank * nw + wib; j < np; j += cpg * nw) s += c4_list16<false>(a, tab, c, U[j], lane);
+    group_barrier(bar, target, cpg);
+    if (static_cast<uint64_t>(np) * 512 >= words) {
+      // big centre: clearing the whole table (16-byte stores) beats walking the lists again
+      uint4* t4 = reinterpret_cast<uint4*>(tab);
+      const uint64_t n4 = words / 4;
+      for (uint64_t i = static_cast<uint64_t>(rank) * blockDim.x + threadIdx.x; i < n4;
+           i += static_cast<uint64_t>(cpg) * blockDim.x)
+        t4[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (rank == 0)
+        for (uint64_t i = n4 * 4 + threadIdx.x; i < words; i += blockDim.x) tab[i] = 0u;
+    } else {
+      for (uint32_t j = rank * nw + wib; j < np; j += cpg * nw) c4_list16<true>(a, tab, c, U[j], lane);
+    }
+    group_barrier(bar, target, cpg);
+  }
+  s = warp_sum(s);
+  if (lane == 0) red[wib] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = static_cast<i128>((static_cast<unsigned __int128>(a.part[2 * blockIdx.x + 1]) << 64) |
+                               a.part[2 * blockIdx.x]);
+    for (int w = 0; w < nw; ++w) t += static_cast<i128>(red[w]);
     a.part[2 * blockIdx.x] = static_cast<ull>(t);
     a.part[2 * blockIdx.x + 1] = static_cast<ull>(t >> 64);
   }
@@ -1801,13 +1904,28 @@ int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st
     if (cudaMemsetAsync(a.next2, 0, sizeof(ull), st) != cudaSuccess) return 1;
     FastArgs w = a;
     w.part = a.part + 2 * blocks * kM4C4;
-    c4_kernel<<<blocks, kC4Threads, 0, st>>>(w);  // stores its partials; the hub launches add to them
+    c4_kernel<<<std::max(1u, std::min(blocks, a.c4_blocks)), kC4Threads, 0, st>>>(w);  // stores its partials; the others add
     for (uint32_t c = 0; c < a.hub_count; ++c) {
       if (a.num_shards > 1 && c % a.num_shards != a.shard) continue;
       c4_hub_kernel<false><<<blocks, kFastThreads, 0, st>>>(w, c);
       c4_hub_kernel<true><<<blocks, kFastThreads, 0, st>>>(w, c);
     }
     if (cudaGetLastError() != cudaSuccess) return 1;
+    if (a.group_end > a.hub_count) {
+      if (cudaMemsetAsync(a.gbar, 0, a.groups * sizeof(ull), st) != cudaSuccess) return 1;
+      // every CTA must be resident (spin barriers): size the grid by occupancy
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c4_group_kernel, kC4Threads, 0);
+      const unsigned fit = std::min<unsigned>(blocks, static_cast<unsigned>(std::max(1, per_sm) * sms));
+      if (fit < a.groups) w.groups = fit;
+      const unsigned grid = (fit / w.groups) * w.groups;
+      void* params[] = {static_cast<void*>(&w)};
+      if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(c4_group_kernel), dim3(grid), dim3(kC4Threads), params,
+                                      0, st) != cudaSuccess)
+        return 1;
+    }
   }
   if (ev) cudaEventRecord(ev[1], st);
   FastArgs w = a;

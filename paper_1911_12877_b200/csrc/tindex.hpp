@@ -55,6 +55,11 @@ struct FastArgs {
   uint32_t shard;                      // this shard (m4_launch: vertices dealt round-robin)
   uint32_t units_per_edge;             // m4_launch: level-1 units per undirected edge (1: v1 < v0, else 2)
   uint32_t hub_count;                  // m4_launch: centres [0, hub_count) take the grid-wide C4 path
+  uint32_t group_end;                  // centres [hub_count, group_end): group tier; the rest one CTA each
+  uint32_t c4_blocks;                  // CTAs (= dense tables) of c4_kernel, <= the launch's blocks
+  uint32_t groups;                     // CTA groups of the group tier (each owns one table of gtab)
+  uint32_t* gtab;                      // groups x ceil(n / 2) words: packed 16-bit counters, zero
+  unsigned long long* gbar;            // groups barrier counters
   const unsigned long long* map_begin;
   const unsigned long long* map_pref;
   uint32_t map_k;
@@ -110,6 +115,7 @@ struct M4Weights {
   }
 };
 bool m4_weights(int kind, M4Weights* w);
+constexpr uint32_t kM4GroupDegree = 512;  // centres from this degree up to the hub degree: group tier
 constexpr uint32_t kM4HubDegree = 16384;  // centres of at least this degree are scattered by the whole grid
 constexpr uint32_t kM4MaxHubs = 16384;
 int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st, cudaEvent_t* ev);

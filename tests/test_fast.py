@@ -157,10 +157,13 @@ def test_count_many_shares_work_and_matches_single_counts(spec, port):
 
 
 @pytest.mark.gpu
-def test_four_cycle_hub_path_in_subprocess():
-    """The grid-wide scatter of hub centres (c4_hub_kernel) only engages from
-    degree 16384; SMG_M4_HUB_DEGREE=6 (read when the library loads) sends most
-    centres of a small graph through it.  Totals and 3-shard sums must equal the
+@pytest.mark.parametrize("hub,group", [("6", "512"), ("64", "3"), ("100000", "0")])
+def test_four_cycle_hub_path_in_subprocess(hub, group):
+    """The tiers of the 4-cycle pass engage by degree: the grid-wide scatter of
+    hub centres (c4_hub_kernel) from 16384, the group tier (c4_group_kernel,
+    L2-resident 16-bit tables, group barriers) from 512.  SMG_M4_HUB_DEGREE /
+    SMG_M4_GROUP_DEGREE (read when the library loads) send the centres of a
+    small graph through each of them.  Totals and 3-shard sums must equal the
     generic executor's."""
     import os
     import subprocess
@@ -178,6 +181,7 @@ for p in plans:
     assert sum(count_shard(g, p, i, 3).count for i in range(3)) == want
 print("hub path OK")
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    p = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SMG_M4_HUB_DEGREE="6"),
+    p = subprocess.run([sys.executable, "-c", code],
+                       env=dict(os.environ, SMG_M4_HUB_DEGREE=hub, SMG_M4_GROUP_DEGREE=group),
                        capture_output=True, text=True, timeout=900)
     assert p.returncode == 0 and "hub path OK" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]

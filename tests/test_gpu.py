@@ -247,6 +247,15 @@ def test_big_config_reference_roots(cfg):
             continue
         got = [count_range(g, plan, v, v + 1).count for v in rec["roots"]]
         assert got == rec["counts"], (cfg, label)
+    # top-degree and 99.9th-percentile roots (tools/ref_roots.py): the CTA tier,
+    # radix index and bitmap slicing of the generic executor, and the folded
+    # per-unit kernels, on the hub-heavy units of the large configs
+    for label, plan in configs.config_patterns(cfg):
+        rec = gold[cfg].get("hub_roots", {}).get(label)
+        if not rec or not rec["roots"]:
+            continue
+        got = [count_range(g, plan, v, v + 1).count for v in rec["roots"]]
+        assert got == rec["counts"], (cfg, label, "hub roots")
 
 
 def test_enumerate_matches_reference(golden, corpus_graphs):
