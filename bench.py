@@ -294,9 +294,13 @@ def load_profile(cfg, kernel):
     if not hit:
         return None
     l2b = sum(p["l2_bytes"] for p in hit)
-    return {"dram_bytes": sum(p["dram_bytes"] for p in hit),
-            "l2_hit_pct": (sum((p["l2_hit_pct"] or 0) * p["l2_bytes"] for p in hit) / l2b) if l2b else None,
-            "launches": sum(p["launches"] for p in hit), "source": ent.get("source")}
+    out = {"dram_bytes": sum(p["dram_bytes"] for p in hit),
+           "l2_hit_pct": (sum((p["l2_hit_pct"] or 0) * p["l2_bytes"] for p in hit) / l2b) if l2b else None,
+           "launches": sum(p["launches"] for p in hit), "source": ent.get("source")}
+    for k in ("sm_throughput_pct", "l2_throughput_pct", "warps_active_pct", "full_capture"):
+        if k in hit[0]:
+            out[k] = hit[0][k]  # from the kernel's ncu --set full capture
+    return out
 
 
 # kernels one full count launches: the generic executor runs count_kernel (+
@@ -532,6 +536,12 @@ def our_arm(args):
                          "kernel": dom, "kernel_ms_per_step": dom_ms, "kernel_ms_all": kernel_ms,
                          "kernel_launches_per_step": prof.get("launches") if prof else None,
                          "l2_hit_pct": prof.get("l2_hit_pct") if prof else None,
+                         "sm_throughput_pct": prof.get("sm_throughput_pct") if prof else None,
+                         "l2_throughput_pct": prof.get("l2_throughput_pct") if prof else None,
+                         "note": ("frac is the dominant kernel's DRAM traffic over its live time over the "
+                                  "measured HBM peak; a low value with a high L2 hit rate means the kernel is "
+                                  "not HBM-bound (sm_throughput_pct / l2_throughput_pct, from its ncu --set "
+                                  "full capture, say what it is bound by)"),
                          "peak_source": peak_kind,
                          "traffic_source": prof.get("source") if prof else None,
                          "algorithmic": {"value": alg_gbs, "unit": "GB/s",

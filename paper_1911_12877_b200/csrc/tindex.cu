@@ -1758,9 +1758,11 @@ __global__ void __launch_bounds__(kC4Threads, 2) c4_group_kernel(const FastArgs 
   uint32_t* tab = a.gtab + static_cast<uint64_t>(g) * words;
   ull* bar = a.gbar + g;
   ull target = 0, s = 0;
-  for (uint64_t c64 = static_cast<uint64_t>(a.hub_count) + g; c64 < a.group_end; c64 += a.groups) {
+  // the shard's centres c = shard (mod num_shards) of the tier, dealt round-robin to the groups
+  const uint64_t S = a.num_shards > 1 ? a.num_shards : 1;
+  const uint64_t first = a.hub_count + (S + (a.num_shards > 1 ? a.shard : 0) - a.hub_count % S) % S;
+  for (uint64_t c64 = first + g * S; c64 < a.group_end; c64 += a.groups * S) {
     const uint32_t c = static_cast<uint32_t>(c64);
-    if (!owns_vertex(a, c)) continue;
     const ull co = a.off[c];
     const uint32_t dc = static_cast<uint32_t>(a.off[c + 1] - co);
     const uint32_t k0 = lb32(a.adj + co, dc, c + 1u);

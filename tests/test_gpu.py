@@ -214,6 +214,20 @@ def test_cfg2_full_clique4_vs_reference(golden_configs, cfg2):
     assert count(cfg2, named_plan("clique", 4)) == full["count"]
 
 
+def test_cfg2_full_rectangle_vs_reference(golden_configs, cfg2):
+    """The headline's dominant pattern against the reference's own full count
+    (tools/ref_full.py cfg2 rectangle: Executor::count_range over every root
+    chunk, ~2e5 core-seconds): the closed form on the relabelled copy (default),
+    the generic executor on the caller's labels, and the per-unit fold."""
+    full = golden_configs["cfg2"]["full"].get("rectangle")
+    if not full:
+        pytest.skip("full reference count not generated (tools/ref_full.py cfg2 rectangle)")
+    p = named_plan("rectangle")
+    assert count(cfg2, p) == full["count"]
+    assert count_result(cfg2, p, generic=True).count == full["count"]
+    assert sum(count_shard(cfg2, p, i, 3).count for i in range(3)) == full["count"]
+
+
 def test_cfg2_full_size_invariants(cfg2):
     p = named_plan("clique", 4)
     full = count_result(cfg2, p)

@@ -15,3 +15,23 @@ for r in count_clique4 c4group m4edge; do
 done
 cp $G/r02_bench_cfg2.json profiles/r02_bench_cfg2.json
 ls -la profiles | grep r02
+# merge the --set full utilisation figures into ncu_summary.json (bench.py copies them into the roofline object)
+python - <<'PY'
+import json
+doc = json.load(open("profiles/ncu_summary.json"))
+per = doc["workloads"]["cfg2:step"]["per_kernel"]
+for kernel, rep in (("count_kernel", "count_clique4"), ("c4_group_kernel", "c4group"), ("m4_edge_kernel", "m4edge")):
+    try:
+        rec = json.load(open(f"profiles/r02_ncu_{rep}_cfg2.json"))[0]
+    except Exception:
+        continue
+    if kernel in per:
+        for key, name in (("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_throughput_pct"),
+                          ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_throughput_pct"),
+                          ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active_pct"),
+                          ("launch__registers_per_thread", "registers_per_thread")):
+            if key in rec:
+                per[kernel][name] = float(rec[key]["value"])
+        per[kernel]["full_capture"] = f"profiles/r02_{rep}_cfg2.ncu-rep"
+json.dump(doc, open("profiles/ncu_summary.json", "w"), indent=1)
+PY
