@@ -289,7 +289,8 @@ def load_profile(cfg, kernel):
     if not ent:
         return None
     per = ent.get("per_kernel", {})
-    names = ["c4_kernel", "c4_hub_kernel", "c4_group_kernel"] if kernel == "c4_kernel" else [kernel]
+    names = {"c4_kernel": ["c4_kernel", "c4_hub_kernel", "c4_group_kernel"],
+             "k4_cta_kernel": ["k4_cta_kernel", "k4_warp_kernel", "count_kernel", "heavy_kernel"]}.get(kernel, [kernel])
     hit = [per[n] for n in names if n in per]
     if not hit:
         return None
@@ -298,8 +299,10 @@ def load_profile(cfg, kernel):
            "l2_hit_pct": (sum((p["l2_hit_pct"] or 0) * p["l2_bytes"] for p in hit) / l2b) if l2b else None,
            "launches": sum(p["launches"] for p in hit), "source": ent.get("source")}
     for k in ("sm_throughput_pct", "l2_throughput_pct", "warps_active_pct", "full_capture"):
-        if k in hit[0]:
-            out[k] = hit[0][k]  # from the kernel's ncu --set full capture
+        for p in hit:
+            if k in p:
+                out[k] = p[k]  # from the ncu --set full capture of the phase's main kernel
+                break
     return out
 
 
@@ -417,7 +420,7 @@ def our_arm(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     kern_ms = {label: [] for label, _ in plans}
-    phase_ms = [[], [], [], []]  # per timed step: count_kernel (K4), c4 pass, edge pass, vertex pass
+    phase_ms = [[], [], [], []]  # per timed step: 4-clique count (k4.cu), c4 pass, edge pass, vertex pass
     for _ in range(args.warmup):
         step(h)
         flush.add_(1)
@@ -489,7 +492,7 @@ def our_arm(args):
     step_kernel_ms = sum(statistics.mean(v) for v in kern_ms.values())
     alg_gbs = 4.0 * E_total / (step_kernel_ms / 1e3) / 1e9 if metered and world == 1 else None
     peak, peak_kind = load_peaks()
-    phase_names = ["count_kernel", "c4_kernel", "m4_edge_kernel", "m4_vertex_kernel"]
+    phase_names = ["k4_cta_kernel", "c4_kernel", "m4_edge_kernel", "m4_vertex_kernel"]
     if any(statistics.mean(v) > 0 for v in phase_ms):
         kernel_ms = {nm: statistics.mean(v) for nm, v in zip(phase_names, phase_ms)}
     else:  # no closed-form batch in this config: one kernel_ms per count

@@ -32,6 +32,7 @@
 
 #include "../../include/symmine_gpu.h"
 #include "graph_build.hpp"
+#include "k4.hpp"
 #include "program.hpp"
 #include "tindex.hpp"
 
@@ -2329,6 +2330,7 @@ struct Replica {
   // degree-ordered copy of the CSR (orient_reindex ids: 0 = highest degree),
   // built on first use for the label-free full counts (cliques, 4-cycles)
   DevCSR ocsr;
+  K4Work k4w;                                          // buffers of the per-root 4-clique count (k4.cu)
   bool tiers_valid = false;                            // hub / group tier bounds of the ordered copy
   uint32_t hub_count = 0, group_end = 0;
   uint32_t* gtab = nullptr;                            // group-tier tables of the 4-cycle pass
@@ -2878,6 +2880,12 @@ const int g_relabel = [] {
   return (e && *e == '0') ? 0 : 1;
 }();
 
+// SMG_K4=0: count 4-cliques through the generic executor instead of k4.cu.
+const int g_k4 = [] {
+  const char* e = std::getenv("SMG_K4");
+  return (e && *e == '0') ? 0 : 1;
+}();
+
 // SMG_M4_HUB_DEGREE: degree from which a centre of the 4-cycle pass is scattered
 // by the whole grid (tests lower it so small graphs take the hub path).
 const uint32_t g_m4_hub = [] {
@@ -2959,13 +2967,22 @@ struct OrientedView {
 // 1: clique plan (generic executor on the oriented view); 2: the 4-vertex
 // kinds with a closed form over subgraph counts (m4_launch); 0: keep the
 // caller's labelling.
+// A fully restricted 4-clique plan (v0 > v1 > v2 > v3: each 4-clique once).
+bool clique4_plan(const smg_plan& p) {
+  return p.depth == 4 && clique_plan(p) && p.parent[1] == 0 && p.parent[2] == 1 && p.parent[3] == 2;
+}
+
 int relabel_mode(const smg_plan& plan, uint32_t flags) {
   if (!g_relabel || (flags & (SMG_METER | SMG_GENERIC))) return 0;
+  if (g_fast && g_k4 && clique4_plan(plan)) return 2;  // K4 itself: the per-root count of k4.cu
   if (clique_plan(plan)) return 1;
   if (!g_fast) return 0;
   M4Weights w;
   return m4_weights(fast_kind(plan), &w) ? 2 : 0;
 }
+
+// The closed-form kind of a plan relabel_mode() sends to m4_count.
+int m4_kind(const smg_plan& plan) { return clique4_plan(plan) ? kFastClique4 : fast_kind(plan); }
 
 int enqueue_oriented(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
   int rc = ensure_oriented(g, r);
@@ -2997,10 +3014,21 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
     if (!m4_weights(kinds[i], &W[i])) return fail(SMG_EIO, "internal: kind has no closed form");
     need |= W[i].need();
   }
-  // K4 share: the clique plan v0 > v1 > v2 > v3 through the generic executor
-  unsigned long long k4 = 0;
+  // K4 share: per-root local-graph count on the ordered copy (k4.cu); the
+  // clique plan v0 > v1 > v2 > v3 through the generic executor when a root's
+  // list exceeds that kernel's capacity, or with SMG_K4=0
+  unsigned long long k4 = 0, k4_units = 0;
   double k4_ms = 0;
-  {
+  bool k4_done = false;
+  if (g_k4) {
+    std::string kerr;
+    const int krc = k4_count(r.off, r.adj, g.n, L.shard, L.num_shards, r.num_sms, r.active(), &r.k4w, &k4,
+                             &k4_units, &k4_ms, &kerr);
+    if (krc == 1) return fail(SMG_EIO, kerr);
+    if (krc == 3) return fail(SMG_EOVERFLOW, "4-clique count exceeds 64 bits");
+    k4_done = krc == 0;
+  }
+  if (!k4_done) {
     smg_plan p;
     std::memset(&p, 0, sizeof(p));
     p.depth = 4;
@@ -3024,6 +3052,7 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
     if (rc) return rc;
     if (ovf) return fail(SMG_EOVERFLOW, "4-clique count exceeds 64 bits");
     k4 = c;
+    k4_units = u;
   }
   cudaStream_t st = r.active();
   const unsigned blocks = static_cast<unsigned>(r.num_sms) * 2;
@@ -3107,7 +3136,7 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
     a.group_end = r.group_end;
     if (a.group_end > a.hub_count) {
       // as many group tables as stay L2-resident together (about 64 MB), at most 16
-      const size_t table = ((g.n + 1) / 2) * sizeof(uint32_t);
+      const size_t table = m4_group_table_words(g.n) * sizeof(uint32_t);
       const uint32_t groups = static_cast<uint32_t>(std::min<size_t>(16, std::max<size_t>(1, (64u << 20) / table)));
       const size_t need_bytes = groups * table;
       if (need_bytes > r.gtab_bytes) {
@@ -3136,8 +3165,10 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   SMG_CUDA(cudaEventRecord(r.ev0, st));
   for (cudaEvent_t& e : r.phase_ev)
     if (!e) SMG_CUDA(cudaEventCreate(&e));
-  if (g.slots && m4_launch(a, need, blocks, st, r.phase_ev))
+  if (g.slots && need && m4_launch(a, need, blocks, st, r.phase_ev))
     return fail(SMG_EIO, "4-vertex closed-form kernel launch failed");
+  if (!(g.slots && need))
+    for (cudaEvent_t e : r.phase_ev) SMG_CUDA(cudaEventRecord(e, st));
   SMG_CUDA(cudaGetLastError());
   SMG_CUDA(cudaEventRecord(r.ev1, st));
   SMG_CUDA(cudaMemcpyAsync(r.part_host, r.part_dev, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -3148,13 +3179,13 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   r.phase_ms[0] = k4_ms;
   for (int q = 0; q < 3; ++q) {
     float pt = 0.f;
-    if (g.slots) SMG_CUDA(cudaEventElapsedTime(&pt, r.phase_ev[q], r.phase_ev[q + 1]));
+    SMG_CUDA(cudaEventElapsedTime(&pt, r.phase_ev[q], r.phase_ev[q + 1]));
     r.phase_ms[q + 1] = pt;
   }
   __int128 S[kM4Regions];
   for (int q = 0; q < kM4Regions; ++q) {
     S[q] = 0;
-    if (!g.slots) continue;
+    if (!g.slots || !need) continue;
     for (unsigned b = 0; b < blocks; ++b) {
       const size_t i = 2 * (static_cast<size_t>(q) * blocks + b);
       S[q] += static_cast<__int128>((static_cast<unsigned __int128>(r.part_host[i + 1]) << 64) | r.part_host[i]);
@@ -3169,7 +3200,7 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
     __int128 v = static_cast<__int128>(k4) * W[i].k4;
     for (int q = 0; q < kM4Regions; ++q) v += S[q] * W[i].w[q];
     out[i].share = v;
-    out[i].units = r.host_ctr->units * (plans[i]->parent[1] == 0 ? 1u : 2u);
+    out[i].units = (need ? r.host_ctr->units : k4_units) * (plans[i]->parent[1] == 0 ? 1u : 2u);
     out[i].ms = (static_cast<double>(t) + k4_ms) / np;
   }
   return SMG_OK;
@@ -3343,6 +3374,7 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->fast_dense) cudaFree(r->fast_dense);
     if (r->gtab) cudaFree(r->gtab);
     if (r->gbar) cudaFree(r->gbar);
+    k4_free(&r->k4w);
     if (r->ocsr.off) cudaFree(r->ocsr.off);
     if (r->ocsr.adj) cudaFree(r->ocsr.adj);
     if (r->ocsr.src) cudaFree(r->ocsr.src);
@@ -3644,7 +3676,8 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
   const int rm = relabel_mode(*plan, flags);
   if (rm == 2) {
     M4Out o;
-    rc = m4_count(*g, r, &fk, &plan, 1, L, &o);
+    const int mk = m4_kind(*plan);
+    rc = m4_count(*g, r, &mk, &plan, 1, L, &o);
     if (rc) return rc;
     m4_store(o, out);
     out->wall_ms = now_ms() - t0;
@@ -3864,7 +3897,8 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
   const int fk = fast_for(*plan, flags);
   const int rm = relabel_mode(*plan, flags);
   if (rm == 2) {
-    rc = m4_count_devices(g, &fk, &plan, 1, num_gpus, out);
+    const int mk = m4_kind(*plan);
+    rc = m4_count_devices(g, &mk, &plan, 1, num_gpus, out);
     out->wall_ms = now_ms() - t0;
     return rc;
   }
@@ -3923,10 +3957,9 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
 // kFastClique4 for a fully restricted 4-clique plan (its count is the K4 the
 // closed forms need anyway), or 0 (counted on its own).
 static int batch_kind(const smg_plan& p, uint32_t flags) {
-  if (relabel_mode(p, flags) == 2) return fast_kind(p);
+  if (relabel_mode(p, flags) == 2) return m4_kind(p);
   if (!g_relabel || !g_fast || (flags & (SMG_METER | SMG_GENERIC))) return 0;
-  if (p.depth == 4 && clique_plan(p) && p.parent[1] == 0 && p.parent[2] == 1 && p.parent[3] == 2) return kFastClique4;
-  return 0;
+  return clique4_plan(p) ? kFastClique4 : 0;  // SMG_K4=0: still shares the batch's generic K4
 }
 
 // shard_mode: one shard on one replica (smg_count_many_shard), else the first

@@ -1754,7 +1754,7 @@ __global__ void __launch_bounds__(kC4Threads, 2) c4_group_kernel(const FastArgs 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned cpg = gridDim.x / a.groups;  // the launch makes gridDim.x = groups x cpg
   const unsigned g = blockIdx.x / cpg, rank = blockIdx.x % cpg;
-  const uint64_t words = (a.n + 1) / 2;
+  const uint64_t words = m4_group_table_words(a.n);  // a multiple of 4: tables stay 16-byte aligned
   uint32_t* tab = a.gtab + static_cast<uint64_t>(g) * words;
   ull* bar = a.gbar + g;
   ull target = 0, s = 0;

@@ -58,7 +58,7 @@ struct FastArgs {
   uint32_t group_end;                  // centres [hub_count, group_end): group tier; the rest one CTA each
   uint32_t c4_blocks;                  // CTAs (= dense tables) of c4_kernel, <= the launch's blocks
   uint32_t groups;                     // CTA groups of the group tier (each owns one table of gtab)
-  uint32_t* gtab;                      // groups x ceil(n / 2) words: packed 16-bit counters, zero
+  uint32_t* gtab;                      // groups x m4_group_table_words(n): packed 16-bit counters, zero
   unsigned long long* gbar;            // groups barrier counters
   const unsigned long long* map_begin;
   const unsigned long long* map_pref;
@@ -115,6 +115,8 @@ struct M4Weights {
   }
 };
 bool m4_weights(int kind, M4Weights* w);
+// words of one group-tier table: packed 16-bit counters, padded to 16 bytes
+__host__ __device__ constexpr uint64_t m4_group_table_words(uint64_t n) { return (((n + 1) / 2) + 3) & ~3ull; }
 constexpr uint32_t kM4GroupDegree = 512;  // centres from this degree up to the hub degree: group tier
 constexpr uint32_t kM4HubDegree = 16384;  // centres of at least this degree are scattered by the whole grid
 constexpr uint32_t kM4MaxHubs = 16384;

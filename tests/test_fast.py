@@ -185,3 +185,19 @@ print("hub path OK")
                        env=dict(os.environ, SMG_M4_HUB_DEGREE=hub, SMG_M4_GROUP_DEGREE=group),
                        capture_output=True, text=True, timeout=900)
     assert p.returncode == 0 and "hub path OK" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p,seed", [(600, 0.5, 7), (1500, 0.8, 8), (3000, 0.02, 9)])
+def test_k4_kernel_tiers(n, p, seed):
+    """The per-root 4-clique count (csrc/k4.cu) against the generic executor:
+    warp tier (lists <= 32), CTA tier with rows in shared memory (<= 512) and in
+    the global scratch (dense graph, lists up to ~1,400); shard shares sum up."""
+    g = Graph.from_edges(*er_graph(n, p, seed))
+    plan = named_plan("clique", 4)
+    want = count_result(g, plan, generic=True)
+    got = count_result(g, plan)
+    assert (got.count, got.units) == (want.count, want.units)
+    assert sum(count_shard(g, plan, i, 3).count for i in range(3)) == want.count
+    rect = named_plan("rectangle")
+    assert count_result(g, rect).count == count_result(g, rect, generic=True).count

@@ -7,7 +7,7 @@ G=gpurun_out
 python tools/summarize_launches.py $G/r02_launches_cfg2.csv "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 2 --warmup 1 --no-cpu (cfg2; includes the metering pass: count_kernel<1,...> and heavy_kernel)" > profiles/r02_launches_cfg2.md
 rm -f profiles/ncu_summary.json
 python tools/traffic_summary.py profiles/ncu_summary.json cfg2:step=$G/r02_traffic_cfg2_step.csv > /dev/null
-for r in count_clique4 c4group m4edge; do
+for r in k4cta c4group m4edge; do
   if [ -f $G/r02_${r}_cfg2.ncu-rep ]; then
     cp $G/r02_${r}_cfg2.ncu-rep profiles/
     python tools/ncu_summary.py profiles/r02_${r}_cfg2.ncu-rep profiles/r02_ncu_${r}_cfg2 > /dev/null
@@ -20,7 +20,7 @@ python - <<'PY'
 import json
 doc = json.load(open("profiles/ncu_summary.json"))
 per = doc["workloads"]["cfg2:step"]["per_kernel"]
-for kernel, rep in (("count_kernel", "count_clique4"), ("c4_group_kernel", "c4group"), ("m4_edge_kernel", "m4edge")):
+for kernel, rep in (("k4_cta_kernel", "k4cta"), ("c4_group_kernel", "c4group"), ("m4_edge_kernel", "m4edge")):
     try:
         rec = json.load(open(f"profiles/r02_ncu_{rep}_cfg2.json"))[0]
     except Exception:
