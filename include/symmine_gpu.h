@@ -177,9 +177,10 @@ int smg_count_many_shard(const smg_graph* g, const smg_plan* plans, uint32_t num
 
 /*
  * Device times (CUDA events on the launching stream, ms) of the kernels of the
- * last closed-form 4-vertex count on a replica: ms[0] the 4-clique
- * count_kernel, ms[1] the 4-cycle pass (c4_kernel + hub launches), ms[2]
- * m4_edge_kernel, ms[3] m4_vertex_kernel.  For measurement (bench.py's roofline).
+ * last closed-form 4-vertex count on a replica: ms[0] the 4-clique count
+ * (k4_cta_kernel + k4_warp_kernel, or the generic count_kernel), ms[1] the
+ * 4-cycle pass (c4_group_kernel, c4_hub_kernel launches, c4_kernel), ms[2] the
+ * edge pass, ms[3] m4_vertex_kernel.  For measurement (bench.py's roofline).
  */
 int smg_phase_times(const smg_graph* g, int replica, double* ms);
 

@@ -2331,6 +2331,8 @@ struct Replica {
   // built on first use for the label-free full counts (cliques, 4-cycles)
   DevCSR ocsr;
   K4Work k4w;                                          // buffers of the per-root 4-clique count (k4.cu)
+  uint32_t* tcount = nullptr;                          // per-slot triangle counts it leaves for the edge pass
+  size_t tcount_bytes = 0;
   bool tiers_valid = false;                            // hub / group tier bounds of the ordered copy
   uint32_t hub_count = 0, group_end = 0;
   uint32_t* gtab = nullptr;                            // group-tier tables of the 4-cycle pass
@@ -2380,6 +2382,9 @@ struct WorkSet {
   unsigned long long* part_dev = nullptr;
   unsigned long long* part_host = nullptr;
   size_t part_words = 0;
+  uint32_t* tcount = nullptr;  // per-slot triangle counts (k4.cu -> m4_edge_counts_kernel)
+  size_t tcount_bytes = 0;
+  K4Work k4w;                  // counters, events and row scratch of k4_count (lmax is per graph: reset on adopt)
 };
 std::mutex g_pool_mu;
 WorkSet g_pool[64];  // one parked set per device ordinal
@@ -2397,6 +2402,8 @@ void free_work(WorkSet& w) {
   if (w.gbar) cudaFree(w.gbar);
   if (w.part_dev) cudaFree(w.part_dev);
   if (w.part_host) cudaFreeHost(w.part_host);
+  if (w.tcount) cudaFree(w.tcount);
+  k4_free(&w.k4w);
   w = WorkSet();
 }
 
@@ -2421,6 +2428,12 @@ void park_work(Replica& r) {
   w.part_dev = r.part_dev;
   w.part_host = r.part_host;
   w.part_words = r.part_words;
+  w.tcount = r.tcount;
+  w.tcount_bytes = r.tcount_bytes;
+  r.tcount = nullptr;
+  r.tcount_bytes = 0;
+  w.k4w = r.k4w;
+  r.k4w = K4Work();
   r.fast_dense = nullptr;
   r.gtab = nullptr;
   r.gbar = nullptr;
@@ -2461,6 +2474,10 @@ void adopt_work(Replica& r) {
   r.part_dev = w.part_dev;
   r.part_host = w.part_host;
   r.part_words = w.part_words;
+  r.tcount = w.tcount;
+  r.tcount_bytes = w.tcount_bytes;
+  r.k4w = w.k4w;
+  r.k4w.lmax = 0;  // the longest list is a property of the graph
   w = WorkSet();
   g_pool_used[r.device] = false;
 }
@@ -3020,14 +3037,30 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   unsigned long long k4 = 0, k4_units = 0;
   double k4_ms = 0;
   bool k4_done = false;
+  uint32_t* tcount = nullptr;  // triangles per edge, a by-product of the 4-clique kernels (one shard only)
   if (g_k4) {
+    if (need && L.num_shards <= 1 && g.slots) {
+      const size_t tb = g.slots * sizeof(uint32_t);
+      if (tb > r.tcount_bytes) {
+        if (r.tcount) cudaFree(r.tcount);
+        r.tcount = nullptr;
+        r.tcount_bytes = 0;
+        if (cudaMalloc(&r.tcount, tb) == cudaSuccess) r.tcount_bytes = tb;
+        else cudaGetLastError();  // no room: the edge pass intersects instead
+      }
+      if (r.tcount) {
+        SMG_CUDA(cudaMemsetAsync(r.tcount, 0, tb, r.active()));
+        tcount = r.tcount;
+      }
+    }
     std::string kerr;
-    const int krc = k4_count(r.off, r.adj, g.n, L.shard, L.num_shards, r.num_sms, r.active(), &r.k4w, &k4,
+    const int krc = k4_count(r.off, r.adj, g.n, L.shard, L.num_shards, r.num_sms, r.active(), &r.k4w, tcount, &k4,
                              &k4_units, &k4_ms, &kerr);
     if (krc == 1) return fail(SMG_EIO, kerr);
     if (krc == 3) return fail(SMG_EOVERFLOW, "4-clique count exceeds 64 bits");
     k4_done = krc == 0;
   }
+  if (!k4_done) tcount = nullptr;
   if (!k4_done) {
     smg_plan p;
     std::memset(&p, 0, sizeof(p));
@@ -3115,6 +3148,7 @@ int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* c
   a.shard = L.shard;
   a.units_per_edge = 1;
   a.c4_blocks = c4_blocks;
+  a.tcount = tcount;
   if (need & (1u << kM4C4)) {
     if (!r.tiers_valid) {
       SMG_CUDA(cudaStreamSynchronize(st));
@@ -3375,6 +3409,7 @@ void smg_graph_destroy(smg_graph* g) {
     if (r->gtab) cudaFree(r->gtab);
     if (r->gbar) cudaFree(r->gbar);
     k4_free(&r->k4w);
+    if (r->tcount) cudaFree(r->tcount);
     if (r->ocsr.off) cudaFree(r->ocsr.off);
     if (r->ocsr.adj) cudaFree(r->ocsr.adj);
     if (r->ocsr.src) cudaFree(r->ocsr.src);

@@ -37,8 +37,8 @@ typedef unsigned long long ull;
 constexpr unsigned kAll = 0xffffffffu;
 constexpr int kThreads = 512;
 constexpr uint32_t kMaxL = 12288;   // list capacity of the CTA tier (48 KB of shared memory)
-constexpr uint32_t kSmemL = 512;    // rows of lists up to this length live in shared memory (512 x 17 words)
-constexpr uint32_t kSmemRowWords = 512 * 17;  // with the list: 84 KB per CTA, two CTAs per SM
+constexpr uint32_t kSmemL = 352;    // rows of lists up to this length live in shared memory (352 x 11 words)
+constexpr uint32_t kSmemRowWords = 352 * 11;  // with the list and degrees: 112 KB per CTA, two CTAs per SM
 // ctr layout
 enum { kNextWarp = 0, kNextCta = 1, kCount = 2, kFlags = 3, kLmax = 4, kUnits = 5, kCtrWords = 8 };
 constexpr uint32_t kRootsPerStep = 16;  // roots a CTA takes per queue step
@@ -85,7 +85,8 @@ __global__ void lmax_kernel(const ull* __restrict__ off, const uint32_t* __restr
 
 __global__ void __launch_bounds__(kThreads) k4_warp_kernel(const ull* __restrict__ off,
                                                            const uint32_t* __restrict__ adj, uint64_t n,
-                                                           uint32_t shard, uint32_t num_shards, ull* ctr) {
+                                                           uint32_t shard, uint32_t num_shards, ull* ctr,
+                                                           uint32_t* __restrict__ tcount) {
   const int lane = threadIdx.x & 31;
   ull total = 0, units = 0;
   for (;;) {
@@ -101,7 +102,8 @@ __global__ void __launch_bounds__(kThreads) k4_warp_kernel(const ull* __restrict
       len = lb32(adj + base, static_cast<uint32_t>(off[mine + 1] - base), static_cast<uint32_t>(mine));
     }
     units += len;  // level-1 units (v1 < v0) of the owned roots
-    unsigned todo = __ballot_sync(kAll, len >= 3 && len <= 32);
+    // with tcount, lists of 2 matter too: their one possible local edge is a triangle
+    unsigned todo = __ballot_sync(kAll, len >= (tcount ? 2u : 3u) && len <= 32);
     while (todo) {
       const int r = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -121,8 +123,20 @@ __global__ void __launch_bounds__(kThreads) k4_warp_kernel(const ull* __restrict
         const uint32_t u = __shfl_sync(kAll, x, j);
         if (lane > static_cast<int>(j) && lane < static_cast<int>(l) && xn) {
           const uint32_t p = lb32(X, xn, u);
-          if (p < xn && X[p] == u) row |= 1u << j;
+          if (p < xn && X[p] == u) {
+            row |= 1u << j;
+            if (tcount) atomicAdd(&tcount[(X - adj) + p], 1u);  // triangle {u, x, root}: edge (x, u)
+          }
         }
+      }
+      if (tcount) {
+        // edges (root, L[lane]): the local degree of lane = its row plus the rows that name it
+        uint32_t deg = __popc(row);
+        for (uint32_t j = 1; j < l; ++j) {
+          const uint32_t rj = __shfl_sync(kAll, row, j);
+          if (lane < static_cast<int>(j)) deg += (rj >> lane) & 1u;
+        }
+        if (lane < static_cast<int>(l) && deg) atomicAdd(&tcount[rb + lane], deg);
       }
       uint32_t cnt = 0;
       for (uint32_t j = 0; j + 1 < l; ++j) {
@@ -142,13 +156,15 @@ __global__ void __launch_bounds__(kThreads) k4_warp_kernel(const ull* __restrict
 
 struct CtaShared {
   uint32_t L[kMaxL];
+  uint32_t deg[kMaxL];  // local degrees (only with tcount)
   ull root;
 };
 
 __global__ void __launch_bounds__(kThreads) k4_cta_kernel(const ull* __restrict__ off,
                                                           const uint32_t* __restrict__ adj, uint64_t n,
                                                           uint32_t shard, uint32_t num_shards, ull* ctr,
-                                                          uint32_t* __restrict__ scratch, uint64_t scratch_words) {
+                                                          uint32_t* __restrict__ scratch, uint64_t scratch_words,
+                                                          uint32_t* __restrict__ tcount) {
   extern __shared__ uint32_t dyn[];
   CtaShared& sh = *reinterpret_cast<CtaShared*>(dyn);
   uint32_t* srows = dyn + (sizeof(CtaShared) + 3) / 4;
@@ -176,7 +192,10 @@ __global__ void __launch_bounds__(kThreads) k4_cta_kernel(const ull* __restrict_
       const uint32_t stride = ((l + 31) >> 5) | 1u;  // odd: rows start in different banks
       uint32_t* rows = (l <= kSmemL) ? srows : grows;
       __syncthreads();
-      for (uint32_t i = threadIdx.x; i < l; i += blockDim.x) sh.L[i] = adj[base + i];
+      for (uint32_t i = threadIdx.x; i < l; i += blockDim.x) {
+        sh.L[i] = adj[base + i];
+        sh.deg[i] = 0u;
+      }
       for (uint64_t i = threadIdx.x; i < static_cast<uint64_t>(l) * stride; i += blockDim.x) rows[i] = 0u;
       __syncthreads();
       // rows: row(i) = {j < i : L[j] in N-(L[i])}
@@ -192,7 +211,14 @@ __global__ void __launch_bounds__(kThreads) k4_cta_kernel(const ull* __restrict_
           for (uint32_t k = lo + lane; k < xn; k += 32) {
             const uint32_t u = X[k];
             const uint32_t p = lb32(sh.L, i, u);
-            if (p < i && sh.L[p] == u) atomicOr(&row[p >> 5], 1u << (p & 31));
+            if (p < i && sh.L[p] == u) {
+              atomicOr(&row[p >> 5], 1u << (p & 31));
+              if (tcount) {  // triangle {u, x, root}: edge (x, u) here, edges (root, x), (root, u) below
+                atomicAdd(&tcount[xo + k], 1u);
+                atomicAdd(&sh.deg[p], 1u);
+                atomicAdd(&sh.deg[i], 1u);
+              }
+            }
           }
         } else {
           // walk L[0..i), find each element in N-(x)
@@ -203,13 +229,23 @@ __global__ void __launch_bounds__(kThreads) k4_cta_kernel(const ull* __restrict_
               const uint32_t u = sh.L[j];
               const uint32_t p = lb32(X, xn, u);
               hit = p < xn && X[p] == u;
+              if (hit && tcount) {
+                atomicAdd(&tcount[xo + p], 1u);
+                atomicAdd(&sh.deg[j], 1u);
+              }
             }
             const unsigned m = __ballot_sync(kAll, hit);
-            if (lane == 0 && m) row[j0 >> 5] = m;
+            if (lane == 0 && m) {
+              row[j0 >> 5] = m;
+              if (tcount) atomicAdd(&sh.deg[i], static_cast<uint32_t>(__popc(m)));
+            }
           }
         }
       }
       __syncthreads();
+      if (tcount)
+        for (uint32_t i = threadIdx.x; i < l; i += blockDim.x)
+          if (sh.deg[i]) atomicAdd(&tcount[base + i], sh.deg[i]);
       // local edges (i, j), j < i: popc(row(i) & row(j)) over the words below j.
       // Sub-warp groups of G lanes take one edge each; G covers the row's words.
       uint32_t G = 1;
@@ -264,8 +300,8 @@ void k4_free(K4Work* w) {
 }
 
 int k4_count(const unsigned long long* off, const uint32_t* adj, uint64_t n, uint32_t shard, uint32_t num_shards,
-             int num_sms, cudaStream_t st, K4Work* w, unsigned long long* count, unsigned long long* units,
-             double* ms, std::string* err) {
+             int num_sms, cudaStream_t st, K4Work* w, uint32_t* tcount, unsigned long long* count,
+             unsigned long long* units, double* ms, std::string* err) {
   cudaError_t e = cudaSuccess;
   if (!w->ctr) {
     e = cudaMalloc(&w->ctr, kCtrWords * sizeof(ull));
@@ -307,8 +343,9 @@ int k4_count(const unsigned long long* off, const uint32_t* adj, uint64_t n, uin
     }
   }
   cudaEventRecord(w->ev0, st);
-  k4_cta_kernel<<<blocks, kThreads, smem, st>>>(off, adj, n, shard, num_shards, w->ctr, w->rows, scratch_words);
-  k4_warp_kernel<<<num_sms * 8, kThreads, 0, st>>>(off, adj, n, shard, num_shards, w->ctr);
+  k4_cta_kernel<<<blocks, kThreads, smem, st>>>(off, adj, n, shard, num_shards, w->ctr, w->rows, scratch_words,
+                                                tcount);
+  k4_warp_kernel<<<num_sms * 8, kThreads, 0, st>>>(off, adj, n, shard, num_shards, w->ctr, tcount);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "k4 launch", err);
   cudaEventRecord(w->ev1, st);

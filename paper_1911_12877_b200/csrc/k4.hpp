@@ -23,12 +23,16 @@ struct K4Work {
 // (u, d), u < d, of the owned d (the level-1 units); *ms = device time.
 // The CSR must be sorted; it is meant to be the orient_reindex copy (ids by
 // descending degree), where N-(d) = {u in N(d) : u < d} is short for every d.
+// tcount (may be null; num_shards == 1 only): one word per slot, zeroed by the
+// caller; on return the word of slot (d, u), u < d, holds |N(u) & N(d)|, the
+// triangles on that edge -- every triangle is met once, at its largest vertex,
+// as a local edge of that root, and adds one to each of its three edges.
 // Returns 0, 1 on a CUDA error (*err), 2 if a root's N-(d) exceeds the
 // kernel's capacity (the caller falls back to the generic executor), 3 on
 // 64-bit overflow.
 int k4_count(const unsigned long long* off, const uint32_t* adj, uint64_t n, uint32_t shard, uint32_t num_shards,
-             int num_sms, cudaStream_t st, K4Work* w, unsigned long long* count, unsigned long long* units,
-             double* ms, std::string* err);
+             int num_sms, cudaStream_t st, K4Work* w, uint32_t* tcount, unsigned long long* count,
+             unsigned long long* units, double* ms, std::string* err);
 void k4_free(K4Work* w);
 
 }  // namespace smg

@@ -1873,6 +1873,37 @@ __global__ void __launch_bounds__(kM4EdgeThreads, 2) m4_edge_kernel(const FastAr
   store_partial(w, acc_p4, 0);
 }
 
+// The same sums from per-slot triangle counts the 4-clique kernels left behind
+// (k4.cu, tcount: slot (u, v), v < u, holds t_e): a streaming pass, no
+// intersections.  Single shard only (a shard's K4 roots see only part of t_e).
+__global__ void __launch_bounds__(kFastThreads) m4_edge_counts_kernel(const FastArgs a) {
+  i128 acc_d = 0, acc_t3 = 0, acc_p4 = 0;
+  ull units = 0;
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < a.slots;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t u = a.src[e], v = a.adj[e];
+    if (v >= u) continue;
+    const ull t = a.tcount[e];
+    const ull du = a.off[u + 1] - a.off[u], dv = a.off[v + 1] - a.off[v];
+    units += a.units_per_edge;
+    acc_d += static_cast<i128>(t * (t - 1) / 2);
+    acc_t3 += static_cast<i128>(t);
+    acc_p4 += static_cast<i128>((du - 1) * (dv - 1));
+    if (a.acc0 != nullptr && t) {
+      atomicAdd(&a.acc0[u], t);
+      atomicAdd(&a.acc0[v], t);
+    }
+  }
+  FastArgs w = a;
+  const unsigned B = gridDim.x;
+  w.part = a.part + 2 * B * kM4D;
+  store_partial(w, acc_d, units);
+  w.part = a.part + 2 * B * kM4T3;
+  store_partial(w, acc_t3, 0);
+  w.part = a.part + 2 * B * kM4P4E;
+  store_partial(w, acc_p4, 0);
+}
+
 // Per owned vertex v: (d_v - 2) t_v and C(d_v, 3), t_v = tv[v] / 2 (0 when
 // a.acc0 is not given); tv is zeroed again.
 __global__ void __launch_bounds__(kFastThreads) m4_vertex_kernel(const FastArgs a) {
@@ -1932,7 +1963,8 @@ int m4_launch(const FastArgs& a, unsigned need, unsigned blocks, cudaStream_t st
   if (ev) cudaEventRecord(ev[1], st);
   FastArgs w = a;
   if (!(need & (1u << kM4Paw))) w.acc0 = nullptr;  // no per-vertex triangle counts needed
-  m4_edge_kernel<<<blocks, kM4EdgeThreads, 0, st>>>(w);
+  if (a.tcount != nullptr && a.num_shards <= 1) m4_edge_counts_kernel<<<blocks, kFastThreads, 0, st>>>(w);
+  else m4_edge_kernel<<<blocks, kM4EdgeThreads, 0, st>>>(w);
   if (cudaGetLastError() != cudaSuccess) return 1;
   if (ev) cudaEventRecord(ev[2], st);
   if (need & ((1u << kM4Paw) | (1u << kM4Star))) {

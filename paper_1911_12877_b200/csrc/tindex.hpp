@@ -57,6 +57,7 @@ struct FastArgs {
   uint32_t hub_count;                  // m4_launch: centres [0, hub_count) take the grid-wide C4 path
   uint32_t group_end;                  // centres [hub_count, group_end): group tier; the rest one CTA each
   uint32_t c4_blocks;                  // CTAs (= dense tables) of c4_kernel, <= the launch's blocks
+  const uint32_t* tcount;              // per-slot triangle counts from k4_count (or null: m4_edge_kernel intersects)
   uint32_t groups;                     // CTA groups of the group tier (each owns one table of gtab)
   uint32_t* gtab;                      // groups x m4_group_table_words(n): packed 16-bit counters, zero
   unsigned long long* gbar;            // groups barrier counters
