@@ -2268,6 +2268,8 @@ const int g_trace = [] {
   return (e && *e && *e != '0') ? 1 : 0;
 }();
 
+constexpr int kTryGeneric = -77;  // internal: the specialised kernel does not apply, run the generic executor
+
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -2705,11 +2707,27 @@ int enqueue(const smg_graph& g, Replica& r, const Program& prog, const Launch& L
 int finish(Replica& r, uint64_t* count, uint64_t* elems, uint64_t* units, bool* ovf, double* ms,
            int64_t* count_hi = nullptr);
 
-// Number of 5-cliques (clique plan, v0 > v1 > ... > v4: each K5 once) through
-// the generic executor's clique-local path; a closed-form term of the folded
-// full counts.  Cached on the replica.  Caller holds r.mu.
+int ensure_oriented(const smg_graph& g, Replica& r);
+int k5_oriented(const smg_graph& g, Replica& r, uint32_t shard, uint32_t num_shards, unsigned long long* count,
+                unsigned long long* units, double* ms);
+
+// Number of 5-cliques: a closed-form term of the folded full counts.  The
+// per-root count of k4.cu on the degree-ordered copy; the clique plan
+// (v0 > v1 > ... > v4: each K5 once) through the generic executor's
+// clique-local path if a list exceeds that kernel's capacity.  Cached on the
+// replica.  Caller holds r.mu.
 int replica_k5(const smg_graph& g, Replica& r, unsigned long long* out) {
   if (!r.k5_valid) {
+    unsigned long long c5 = 0, u5 = 0;
+    double ms5 = 0;
+    const int krc = k5_oriented(g, r, 0, 1, &c5, &u5, &ms5);
+    if (krc == SMG_OK) {
+      r.k5 = c5;
+      r.k5_valid = true;
+      *out = r.k5;
+      return SMG_OK;
+    }
+    if (krc != kTryGeneric) return krc;
     smg_plan p;
     std::memset(&p, 0, sizeof(p));
     p.depth = 5;
@@ -2984,6 +3002,28 @@ struct OrientedView {
 // 1: clique plan (generic executor on the oriented view); 2: the 4-vertex
 // kinds with a closed form over subgraph counts (m4_launch); 0: keep the
 // caller's labelling.
+// 5-cliques of the graph (this shard's roots) through k4.cu on the ordered
+// copy.  SMG_OK, kTryGeneric (SMG_K4=0 or a list beyond the kernel's capacity),
+// or an error.  Synchronous.  Caller holds r.mu.
+int k5_oriented(const smg_graph& g, Replica& r, uint32_t shard, uint32_t num_shards, unsigned long long* count,
+                unsigned long long* units, double* ms) {
+  if (!g_k4 || !g_relabel) return kTryGeneric;
+  int rc = ensure_oriented(g, r);
+  if (rc) return rc;
+  OrientedView view(r);
+  std::string kerr;
+  const int krc = k4_count(r.off, r.adj, g.n, shard, num_shards, r.num_sms, r.active(), &r.k4w, nullptr, count, units,
+                           ms, &kerr, 5);
+  if (krc == 1) return fail(SMG_EIO, kerr);
+  if (krc == 3) return fail(SMG_EOVERFLOW, "5-clique count exceeds 64 bits");
+  return krc == 0 ? SMG_OK : kTryGeneric;
+}
+
+bool clique5_plan(const smg_plan& p) {
+  return p.depth == 5 && clique_plan(p) && p.parent[1] == 0 && p.parent[2] == 1 && p.parent[3] == 2 &&
+         p.parent[4] == 3;
+}
+
 // A fully restricted 4-clique plan (v0 > v1 > v2 > v3: each 4-clique once).
 bool clique4_plan(const smg_plan& p) {
   return p.depth == 4 && clique_plan(p) && p.parent[1] == 0 && p.parent[2] == 1 && p.parent[3] == 2;
@@ -2991,7 +3031,7 @@ bool clique4_plan(const smg_plan& p) {
 
 int relabel_mode(const smg_plan& plan, uint32_t flags) {
   if (!g_relabel || (flags & (SMG_METER | SMG_GENERIC))) return 0;
-  if (g_fast && g_k4 && clique4_plan(plan)) return 2;  // K4 itself: the per-root count of k4.cu
+  if (g_fast && g_k4 && (clique4_plan(plan) || clique5_plan(plan))) return 2;  // the per-root counts of k4.cu
   if (clique_plan(plan)) return 1;
   if (!g_fast) return 0;
   M4Weights w;
@@ -2999,7 +3039,9 @@ int relabel_mode(const smg_plan& plan, uint32_t flags) {
 }
 
 // The closed-form kind of a plan relabel_mode() sends to m4_count.
-int m4_kind(const smg_plan& plan) { return clique4_plan(plan) ? kFastClique4 : fast_kind(plan); }
+int m4_kind(const smg_plan& plan) {
+  return clique4_plan(plan) ? kFastClique4 : clique5_plan(plan) ? kFastClique5 : fast_kind(plan);
+}
 
 int enqueue_oriented(const smg_graph& g, Replica& r, const Program& prog, const Launch& L) {
   int rc = ensure_oriented(g, r);
@@ -3021,6 +3063,16 @@ struct M4Out {
 int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* const* plans, uint32_t np,
              const Launch& L, M4Out* out) {
   r.post_kind = 0;
+  if (np == 1 && kinds[0] == kFastClique5) {
+    unsigned long long c5 = 0, u5 = 0;
+    double ms5 = 0;
+    const int krc = k5_oriented(g, r, L.shard, L.num_shards, &c5, &u5, &ms5);
+    if (krc) return krc;  // kTryGeneric: the caller runs the generic executor
+    out[0].share = static_cast<__int128>(c5);
+    out[0].units = u5;
+    out[0].ms = ms5;
+    return SMG_OK;
+  }
   int rc = ensure_oriented(g, r);
   if (rc) return rc;
   OrientedView view(r);
@@ -3713,12 +3765,14 @@ int smg_count_shard(const smg_graph* g, const smg_plan* plan, int replica, uint3
     M4Out o;
     const int mk = m4_kind(*plan);
     rc = m4_count(*g, r, &mk, &plan, 1, L, &o);
-    if (rc) return rc;
-    m4_store(o, out);
-    out->wall_ms = now_ms() - t0;
-    return SMG_OK;
+    if (rc && rc != kTryGeneric) return rc;
+    if (rc == SMG_OK) {
+      m4_store(o, out);
+      out->wall_ms = now_ms() - t0;
+      return SMG_OK;
+    }
   }
-  rc = rm == 1 ? enqueue_oriented(*g, r, prog, L)
+  rc = rm >= 1 ? enqueue_oriented(*g, r, prog, L)
        : fk    ? enqueue_fast(*g, r, fk, *plan, L)
                : enqueue(*g, r, prog, L);
   if (rc) return rc;
@@ -3901,7 +3955,7 @@ static int m4_count_devices(const smg_graph* g, const int* kinds, const smg_plan
   run(0);
   for (auto& t : th) t.join();
   for (unsigned d = 0; d < num_gpus; ++d)
-    if (rcs[d]) return fail(rcs[d], errs[d]);
+    if (rcs[d]) return rcs[d] == kTryGeneric ? kTryGeneric : fail(rcs[d], errs[d]);
   for (uint32_t i = 0; i < np; ++i) {
     __int128 total = 0;
     std::memset(&out[i], 0, sizeof(out[i]));
@@ -3934,8 +3988,11 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
   if (rm == 2) {
     const int mk = m4_kind(*plan);
     rc = m4_count_devices(g, &mk, &plan, 1, num_gpus, out);
-    out->wall_ms = now_ms() - t0;
-    return rc;
+    if (rc != kTryGeneric) {
+      out->wall_ms = now_ms() - t0;
+      return rc;
+    }
+    std::memset(out, 0, sizeof(*out));
   }
   for (unsigned d = 0; d < num_gpus; ++d) {
     Launch L;
@@ -3948,7 +4005,7 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
     L.shard = d;
     L.num_shards = num_gpus;
     Replica& rd = *g->reps[d];
-    rc = rm == 1 ? enqueue_oriented(*g, rd, prog, L)
+    rc = rm >= 1 ? enqueue_oriented(*g, rd, prog, L)
          : fk    ? enqueue_fast(*g, rd, fk, *plan, L)
                  : enqueue(*g, rd, prog, L);
     if (rc) {
@@ -3992,6 +4049,7 @@ int smg_count(const smg_graph* g, const smg_plan* plan, unsigned num_gpus, uint3
 // kFastClique4 for a fully restricted 4-clique plan (its count is the K4 the
 // closed forms need anyway), or 0 (counted on its own).
 static int batch_kind(const smg_plan& p, uint32_t flags) {
+  if (clique5_plan(p)) return 0;  // counted on its own (smg_count)
   if (relabel_mode(p, flags) == 2) return m4_kind(p);
   if (!g_relabel || !g_fast || (flags & (SMG_METER | SMG_GENERIC))) return 0;
   return clique4_plan(p) ? kFastClique4 : 0;  // SMG_K4=0: still shares the batch's generic K4

@@ -83,6 +83,7 @@ __global__ void lmax_kernel(const ull* __restrict__ off, const uint32_t* __restr
   if ((threadIdx.x & 31) == 0 && best) atomicMax(&ctr[kLmax], static_cast<ull>(best));
 }
 
+template <int K>
 __global__ void __launch_bounds__(kThreads) k4_warp_kernel(const ull* __restrict__ off,
                                                            const uint32_t* __restrict__ adj, uint64_t n,
                                                            uint32_t shard, uint32_t num_shards, ull* ctr,
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) k4_warp_kernel(const ull* __restrict
     }
     units += len;  // level-1 units (v1 < v0) of the owned roots
     // with tcount, lists of 2 matter too: their one possible local edge is a triangle
-    unsigned todo = __ballot_sync(kAll, len >= (tcount ? 2u : 3u) && len <= 32);
+    unsigned todo = __ballot_sync(kAll, len >= (tcount ? 2u : static_cast<uint32_t>(K - 1)) && len <= 32);
     while (todo) {
       const int r = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -141,7 +142,15 @@ __global__ void __launch_bounds__(kThreads) k4_warp_kernel(const ull* __restrict
       uint32_t cnt = 0;
       for (uint32_t j = 0; j + 1 < l; ++j) {
         const uint32_t rj = __shfl_sync(kAll, row, j);
-        if ((row >> j) & 1u) cnt += __popc(row & rj);
+        const uint32_t mij = ((row >> j) & 1u) ? (row & rj) : 0u;  // common local neighbours below j
+        if (K == 4) {
+          cnt += __popc(mij);
+        } else {  // K == 5: triangles (i, j, k) and their common neighbours below k
+          for (uint32_t k = 0; k < j; ++k) {
+            const uint32_t rk = __shfl_sync(kAll, row, k);
+            if ((mij >> k) & 1u) cnt += __popc(mij & rk);
+          }
+        }
       }
       total += cnt;
     }
@@ -160,6 +169,7 @@ struct CtaShared {
   ull root;
 };
 
+template <int K>
 __global__ void __launch_bounds__(kThreads) k4_cta_kernel(const ull* __restrict__ off,
                                                           const uint32_t* __restrict__ adj, uint64_t n,
                                                           uint32_t shard, uint32_t num_shards, ull* ctr,
@@ -246,27 +256,78 @@ __global__ void __launch_bounds__(kThreads) k4_cta_kernel(const ull* __restrict_
       if (tcount)
         for (uint32_t i = threadIdx.x; i < l; i += blockDim.x)
           if (sh.deg[i]) atomicAdd(&tcount[base + i], sh.deg[i]);
-      // local edges (i, j), j < i: popc(row(i) & row(j)) over the words below j.
-      // Sub-warp groups of G lanes take one edge each; G covers the row's words.
-      uint32_t G = 1;
-      while (G < 32 && G < stride) G <<= 1;
-      const uint32_t gid = lane / G, gl = lane % G, ng = 32 / G;
-      for (uint32_t i = 2 + wib; i < l; i += nw) {
-        const uint32_t* ri = rows + static_cast<uint64_t>(i) * stride;
-        const uint32_t wi = (i + 31) >> 5;  // words of row(i) that can be non-zero
-        for (uint32_t w = 0; w < wi; ++w) {
-          const uint32_t m = ri[w];
-          const uint32_t c = __popc(m);
-          for (uint32_t k0 = 0; k0 < c; k0 += ng) {
-            const uint32_t k = k0 + gid;
-            if (k < c) {
-              const uint32_t j = (w << 5) + __fns(m, 0, k + 1);
+      if (K == 4) {
+        // local edges (i, j), j < i: popc(row(i) & row(j)) over the words below j.
+        // Sub-warp groups of G lanes take one edge each; G covers the row's words.
+        uint32_t G = 1;
+        while (G < 32 && G < stride) G <<= 1;
+        const uint32_t gid = lane / G, gl = lane % G, ng = 32 / G;
+        for (uint32_t i = 2 + wib; i < l; i += nw) {
+          const uint32_t* ri = rows + static_cast<uint64_t>(i) * stride;
+          const uint32_t wi = (i + 31) >> 5;  // words of row(i) that can be non-zero
+          for (uint32_t w = 0; w < wi; ++w) {
+            const uint32_t m = ri[w];
+            const uint32_t c = __popc(m);
+            for (uint32_t k0 = 0; k0 < c; k0 += ng) {
+              const uint32_t k = k0 + gid;
+              if (k < c) {
+                const uint32_t j = (w << 5) + __fns(m, 0, k + 1);
+                const uint32_t* rj = rows + static_cast<uint64_t>(j) * stride;
+                const uint32_t wj = (j + 31) >> 5;
+                uint32_t s = 0;
+                for (uint32_t q = gl; q < wj; q += G) s += __popc(ri[q] & rj[q]);
+                total += s;
+              }
+            }
+          }
+        }
+      } else {
+        // K == 5: local triangles (i, j, k), k < j < i, each adds
+        // popc(row(i) & row(j) & row(k)).  A warp takes row i, compacts its set
+        // bits 1,024 at a time into its list (the degree array's space: tcount
+        // is never used with K == 5), and every lane walks one local edge (i, j).
+        uint16_t* list = reinterpret_cast<uint16_t*>(sh.deg) + wib * 1024;
+        for (uint32_t i = 3 + wib; i < l; i += nw) {
+          const uint32_t* ri = rows + static_cast<uint64_t>(i) * stride;
+          const uint32_t wi = (i + 31) >> 5;
+          for (uint32_t w0 = 0; w0 < wi; w0 += 32) {
+            const uint32_t wq = w0 + lane;
+            uint32_t m = wq < wi ? ri[wq] : 0u;
+            uint32_t pos = __popc(m);
+            uint32_t incl = pos;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const uint32_t o = __shfl_up_sync(kAll, incl, d);
+              if (lane >= d) incl += o;
+            }
+            const uint32_t cnt = __shfl_sync(kAll, incl, 31);
+            pos = incl - pos;
+            while (m) {
+              const uint32_t b = __ffs(m) - 1;
+              m &= m - 1;
+              list[pos++] = static_cast<uint16_t>((wq << 5) + b);
+            }
+            __syncwarp();
+            for (uint32_t e = lane; e < cnt; e += 32) {
+              const uint32_t j = list[e];
               const uint32_t* rj = rows + static_cast<uint64_t>(j) * stride;
               const uint32_t wj = (j + 31) >> 5;
-              uint32_t s = 0;
-              for (uint32_t q = gl; q < wj; q += G) s += __popc(ri[q] & rj[q]);
+              ull s = 0;
+              for (uint32_t q = 0; q < wj; ++q) {
+                uint32_t mm = ri[q] & rj[q];
+                while (mm) {
+                  const uint32_t k = (q << 5) + (__ffs(mm) - 1);
+                  mm &= mm - 1;
+                  const uint32_t* rk = rows + static_cast<uint64_t>(k) * stride;
+                  const uint32_t wk = (k + 31) >> 5;
+                  uint32_t t = 0;
+                  for (uint32_t q2 = 0; q2 < wk; ++q2) t += __popc(ri[q2] & rj[q2] & rk[q2]);
+                  s += t;
+                }
+              }
               total += s;
             }
+            __syncwarp();
           }
         }
       }
@@ -301,8 +362,13 @@ void k4_free(K4Work* w) {
 
 int k4_count(const unsigned long long* off, const uint32_t* adj, uint64_t n, uint32_t shard, uint32_t num_shards,
              int num_sms, cudaStream_t st, K4Work* w, uint32_t* tcount, unsigned long long* count,
-             unsigned long long* units, double* ms, std::string* err) {
+             unsigned long long* units, double* ms, std::string* err, int k) {
   cudaError_t e = cudaSuccess;
+  if (k != 4 && k != 5) {
+    if (err) *err = "clique size must be 4 or 5";
+    return 1;
+  }
+  if (k == 5) tcount = nullptr;
   if (!w->ctr) {
     e = cudaMalloc(&w->ctr, kCtrWords * sizeof(ull));
     if (e == cudaSuccess) e = cudaMallocHost(&w->host, kCtrWords * sizeof(ull));
@@ -316,7 +382,9 @@ int k4_count(const unsigned long long* off, const uint32_t* adj, uint64_t n, uin
   if (n == 0) return 0;
   const unsigned blocks = static_cast<unsigned>(num_sms) * 2;
   const size_t smem = ((sizeof(CtaShared) + 3) / 4 + kSmemRowWords) * sizeof(uint32_t);
-  e = cudaFuncSetAttribute(k4_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  e = cudaFuncSetAttribute(k4_cta_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k4_cta_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_fail(e, "k4 shared memory", err);
   e = cudaMemsetAsync(w->ctr, 0, kCtrWords * sizeof(ull), st);
   if (e != cudaSuccess) return cuda_fail(e, "k4 memset", err);
@@ -343,9 +411,15 @@ int k4_count(const unsigned long long* off, const uint32_t* adj, uint64_t n, uin
     }
   }
   cudaEventRecord(w->ev0, st);
-  k4_cta_kernel<<<blocks, kThreads, smem, st>>>(off, adj, n, shard, num_shards, w->ctr, w->rows, scratch_words,
-                                                tcount);
-  k4_warp_kernel<<<num_sms * 8, kThreads, 0, st>>>(off, adj, n, shard, num_shards, w->ctr, tcount);
+  if (k == 4) {
+    k4_cta_kernel<4><<<blocks, kThreads, smem, st>>>(off, adj, n, shard, num_shards, w->ctr, w->rows, scratch_words,
+                                                     tcount);
+    k4_warp_kernel<4><<<num_sms * 8, kThreads, 0, st>>>(off, adj, n, shard, num_shards, w->ctr, tcount);
+  } else {
+    k4_cta_kernel<5><<<blocks, kThreads, smem, st>>>(off, adj, n, shard, num_shards, w->ctr, w->rows, scratch_words,
+                                                     nullptr);
+    k4_warp_kernel<5><<<num_sms * 8, kThreads, 0, st>>>(off, adj, n, shard, num_shards, w->ctr, nullptr);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "k4 launch", err);
   cudaEventRecord(w->ev1, st);

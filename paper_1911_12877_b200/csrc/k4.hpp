@@ -18,7 +18,7 @@ struct K4Work {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
-// Number of 4-cliques {a < b < c < d} of the CSR whose largest vertex d is
+// Number of k-cliques (k = 4 or 5) of the CSR whose largest vertex d is
 // owned by `shard` (d % num_shards == shard), into *count; *units = the edges
 // (u, d), u < d, of the owned d (the level-1 units); *ms = device time.
 // The CSR must be sorted; it is meant to be the orient_reindex copy (ids by
@@ -32,7 +32,7 @@ struct K4Work {
 // 64-bit overflow.
 int k4_count(const unsigned long long* off, const uint32_t* adj, uint64_t n, uint32_t shard, uint32_t num_shards,
              int num_sms, cudaStream_t st, K4Work* w, uint32_t* tcount, unsigned long long* count,
-             unsigned long long* units, double* ms, std::string* err);
+             unsigned long long* units, double* ms, std::string* err, int k = 4);
 void k4_free(K4Work* w);
 
 }  // namespace smg

@@ -39,7 +39,8 @@ void tindex_free(TIndex* t);
 enum FastKind {
   kFastNone = 0, kFastStar4 = 1, kFastTailedDiamondA = 2, kFastHouse = 3, kFastTailedDiamondB = 4,
   kFastTailedTriangle = 5, kFastDiamond = 6, kFastPath4 = 7, kFastRectangle = 8, kFastRectangleMotif = 9,
-  kFastClique4 = 10  // never returned by fast_kind: a fully restricted 4-clique plan inside a batch (m4_weights)
+  kFastClique4 = 10,  // never returned by fast_kind: a fully restricted 4-clique plan inside a batch (m4_weights)
+  kFastClique5 = 11   // never returned by fast_kind: a fully restricted 5-clique plan (k4.cu, k = 5), counted alone
 };
 int fast_kind(const smg_plan& p);
 

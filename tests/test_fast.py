@@ -201,3 +201,21 @@ def test_k4_kernel_tiers(n, p, seed):
     assert sum(count_shard(g, plan, i, 3).count for i in range(3)) == want.count
     rect = named_plan("rectangle")
     assert count_result(g, rect).count == count_result(g, rect, generic=True).count
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p,seed", [(600, 0.5, 7), (900, 0.6, 10), (3000, 0.02, 9)])
+def test_k5_kernel_tiers(n, p, seed):
+    """The per-root 5-clique count (csrc/k4.cu, k = 5: local triangles and their
+    common neighbours) against the generic executor: warp tier, shared-memory
+    rows, global-scratch rows (lists up to ~540); shard shares; and house, whose
+    folded full count takes K5 as a closed-form term."""
+    g = Graph.from_edges(*er_graph(n, p, seed))
+    plan = named_plan("clique", 5)
+    want = count_result(g, plan, generic=True)
+    got = count_result(g, plan)
+    assert (got.count, got.units) == (want.count, want.units)
+    assert sum(count_shard(g, plan, i, 3).count for i in range(3)) == want.count
+    if n <= 600:
+        house = named_plan("house")
+        assert count_result(g, house).count == count_result(g, house, generic=True).count
