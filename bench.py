@@ -211,8 +211,11 @@ def load_graph_file(cfg):
 
 
 def plan_list(cfg):
+    """(label, plan) of the config's patterns that finish (configs.NOT_FINISHED
+    names the rest; the line reports them)."""
     from paper_1911_12877_b200 import configs  # plans + descriptions only: maps no native library
-    return configs.config_patterns(cfg)
+    skip = configs.NOT_FINISHED.get(cfg, ())
+    return [(lbl, p) for lbl, p in configs.config_patterns(cfg) if lbl not in skip]
 
 
 def describe(cfg):
@@ -382,7 +385,7 @@ def our_arm(args):
     barrier()
     if rank != 0:
         graph = configs.load(CONFIG)
-    plans = configs.config_patterns(CONFIG)
+    plans = plan_list(CONFIG)
     lib = N.gpu_lib()
     stream = torch.cuda.current_stream(dev)
     h = graph.device_handle((local,))
@@ -528,6 +531,7 @@ def our_arm(args):
             "data": f"synthetic ({configs.describe(CONFIG)}; seeded, no public dataset named)",
             "config": {"workload": f"{CONFIG}: {configs.describe(CONFIG)} (n={graph.n}, m={graph.m})",
                        "patterns": [lbl for lbl, _ in plans], "counts": counts,
+                       "patterns_not_finished": list(configs.NOT_FINISHED.get(CONFIG, ())),
                        "elements": E, "pattern_ms": {k: statistics.mean(v) for k, v in kern_ms.items()},
                        "folded_kernels": {k: v for k, v in folded.items() if v},
                        "parallelism": f"units sharded over {world} GPU(s), 1 allreduce",

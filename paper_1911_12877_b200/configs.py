@@ -56,6 +56,11 @@ DESCRIPTIONS = {
 }
 
 
+# Patterns no engine here (nor the reference) finishes on their config: left out
+# of bench.py's step and reported in its line.
+NOT_FINISHED = {"cfg5": ("pentagon",)}
+
+
 def describe(cfg: str) -> str:
     return DESCRIPTIONS[cfg]
 
