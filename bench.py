@@ -461,7 +461,7 @@ def our_arm(args):
     adj_pin = torch.from_numpy(graph.adjacency.view(np.int32)).pin_memory()
     h2d = off_pin.numel() * 8 + adj_pin.numel() * 4
     d2h = 48 * len(plans)
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, min(args.steps, 8))
     t_e2e = 0.0
     e2e_parts = {"graph_create_ms": 0.0, "count_ms": 0.0, "graph_destroy_ms": 0.0}
     for s in range(e2e_steps + 1):
