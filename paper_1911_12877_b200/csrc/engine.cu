@@ -3436,7 +3436,10 @@ int smg_plan_describe(const smg_plan* plan, char* buf, size_t cap) {
        ",\"batch_yltx\":" + std::to_string(pr.batch_yltx) +
        ",\"batch_fixed_bound\":" + std::to_string(pr.batch_fixed_bound) +
        ",\"clique\":" + std::to_string(pr.clique) + ",\"fast\":" + std::to_string(fast_kind(*plan)) +
-       ",\"parent\":[";
+       // how a full count runs: 0 caller's labels, 1 generic executor on the degree-ordered copy,
+       // 2 closed form / per-root clique kernel on the copy (full_kind: FastKind incl. 10, 11)
+       ",\"full_count_mode\":" + std::to_string(relabel_mode(*plan, 0)) +
+       ",\"full_kind\":" + std::to_string(relabel_mode(*plan, 0) == 2 ? m4_kind(*plan) : 0) + ",\"parent\":[";
   for (int i = 0; i < pr.depth; ++i) s += (i ? "," : "") + std::to_string(pr.parent[i]);
   s += "]}";
   if (s.size() + 1 > cap) return fail(SMG_EINPUT, "buffer too small");

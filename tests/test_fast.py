@@ -50,6 +50,28 @@ def test_folded_kinds_are_recognised():
         assert describe(r["plan"])["fast"] == MOTIF_KIND.get(r["name"], 0), r["name"]
 
 
+def test_full_count_modes_are_recognised():
+    """Host-only: which plans take the label-free full-count paths (relabel_mode,
+    engine.cu): clique plans run on the degree-ordered copy (the fully restricted
+    4- and 5-clique plans through the per-root kernel of k4.cu), the recognised
+    4-vertex plans through the closed forms; everything else keeps the
+    caller's labels."""
+    fp = folded_plans()
+    for name in ("star4", "tailed_triangle", "diamond", "path4", "rectangle", "rectangle_motif"):
+        d = describe(fp[name])
+        assert (d["full_count_mode"], d["full_kind"]) == (2, FOLDED[name]), name
+    for name in ("house", "tailed_diamond_a", "tailed_diamond_b"):
+        assert describe(fp[name])["full_count_mode"] == 0, name
+    assert describe(named_plan("pentagon"))["full_count_mode"] == 0
+    assert describe(named_plan("triangle"))["full_count_mode"] == 1
+    assert (describe(named_plan("clique", 4))["full_count_mode"], describe(named_plan("clique", 4))["full_kind"]) == (2, 10)
+    assert (describe(named_plan("clique", 5))["full_count_mode"], describe(named_plan("clique", 5))["full_kind"]) == (2, 11)
+    assert describe(named_plan("clique", 6))["full_count_mode"] == 1
+    # partially restricted / unrestricted cliques are label-free too (generic executor on the copy)
+    assert describe(named_plan("clique", 4, use_restrictions=False))["full_count_mode"] == 1
+    assert describe(named_plan("rectangle", use_restrictions=False))["full_count_mode"] == 0
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,p,seed", [(30, 0.3, 1), (40, 0.5, 2), (25, 0.7, 3), (60, 0.15, 4), (80, 0.08, 5)])
 def test_folded_per_root_vs_reference(reference, n, p, seed):
