@@ -28,6 +28,9 @@ ap.add_argument("--hubs", type=int, default=8)
 ap.add_argument("--mid", type=int, default=8, help="roots of degree ~ the 99.9th percentile")
 ap.add_argument("--budget", type=float, default=240.0, help="seconds per root")
 ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+ap.add_argument("--quantile", type=float, default=0.999, help="degree quantile of the mid roots")
+ap.add_argument("--labels", default="", help="comma-separated pattern labels (default: all of the config)")
+ap.add_argument("--append", action="store_true", help="add to the roots already recorded for a label")
 args = ap.parse_args()
 
 gold = json.load(open(PATH))
@@ -38,16 +41,22 @@ for cfg in args.cfgs.split(","):
     deg = np.diff(g.offsets.astype(np.int64))
     order = np.argsort(-deg, kind="stable")
     hubs = [int(v) for v in order[: args.hubs]]
-    q = np.quantile(deg[deg > 0], 0.999)
-    pool = np.flatnonzero((deg >= q) & (deg < deg[hubs[-1]]))
+    q = np.quantile(deg[deg > 0], args.quantile)
+    pool = np.flatnonzero((deg >= q) & (deg < (deg[hubs[-1]] if hubs else deg.max() + 1)) & (deg <= 2 * q))
     rng = np.random.default_rng(99)
     mids = sorted(int(v) for v in rng.choice(pool, size=min(args.mid, pool.size), replace=False))
     entry = gold.setdefault(cfg, {})
     entry.setdefault("hub_roots", {})
     for label, plan in configs.config_patterns(cfg):
+        if args.labels and label not in args.labels.split(","):
+            continue
         pj = plan.to_json()
         roots, counts, degs, secs, dropped = [], [], [], [], []
-        for v in hubs + mids:
+        old = entry["hub_roots"].get(label) if args.append else None
+        if old:
+            roots, counts, degs = list(old["roots"]), list(old["counts"]), list(old["degrees"])
+            secs, dropped = list(old.get("seconds", [])), list(old.get("dropped_over_budget", []))
+        for v in [x for x in hubs + mids if x not in roots]:
             lo, hi = int(g.offsets[v]), int(g.offsets[v + 1])
             v1 = g.adjacency[lo:hi]
             v0 = np.full(v1.size, v, dtype=np.uint32)
