@@ -413,10 +413,16 @@ def our_arm(args):
     folded = {label: kernels_per_count(plan)[1] for label, plan in plans}
     metered = CONFIG in METERED_CONFIGS  # SMG_METER runs the generic executor
     E, counts = {}, {}
-    for label, plan in plans:
-        r = shard(plan, meter=metered)
-        c, e = allsum_u64([(int(r.count_hi) << 64) + int(r.count), r.elements])
-        E[label], counts[label] = (e if metered else None), c
+    if metered:
+        for label, plan in plans:
+            r = shard(plan, meter=True)
+            c, e = allsum_u64([(int(r.count_hi) << 64) + int(r.count), r.elements])
+            E[label], counts[label] = e, c
+    else:  # count-time configs: the reference counts are the first step's (untimed)
+        res0 = step(h)
+        tot = allsum_u64([(int(res0[i].count_hi) << 64) + int(res0[i].count) for i in range(len(plans))])
+        for (label, _), c in zip(plans, tot):
+            E[label], counts[label] = None, c
     E_total = sum(E.values()) if metered else None
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
@@ -424,7 +430,7 @@ def our_arm(args):
           for _ in range(args.steps)]
     kern_ms = {label: [] for label, _ in plans}
     phase_ms = [[], [], [], []]  # per timed step: 4-clique count (k4.cu), c4 pass, edge pass, vertex pass
-    for _ in range(args.warmup):
+    for _ in range(args.warmup if metered else max(0, args.warmup - 1)):  # the count pass above warmed one
         step(h)
         flush.add_(1)
     torch.cuda.synchronize(dev)
@@ -464,7 +470,12 @@ def our_arm(args):
     e2e_steps = max(1, min(args.steps, 8))
     t_e2e = 0.0
     e2e_parts = {"graph_create_ms": 0.0, "count_ms": 0.0, "graph_destroy_ms": 0.0}
-    for s in range(e2e_steps + 1):
+    # the first iteration warms the allocator / context and is not timed, unless a
+    # step takes minutes (then one iteration, timed, is all the budget allows)
+    e2e_warm = 0 if t_step > 30.0 else 1
+    if not e2e_warm:
+        e2e_steps = 1
+    for s in range(e2e_steps + e2e_warm):
         barrier()
         t0 = time.perf_counter()
         gh = ctypes.c_void_p()
@@ -478,7 +489,7 @@ def our_arm(args):
         t2 = time.perf_counter()
         lib.smg_graph_destroy(gh)
         t3 = time.perf_counter()
-        if s > 0:  # first iteration warms the allocator / context
+        if s >= e2e_warm:
             t_e2e += t3 - t0
             for k, v in zip(e2e_parts, (t1 - t0, t2 - t1, t3 - t2)):
                 e2e_parts[k] += 1e3 * v / e2e_steps

@@ -3008,6 +3008,7 @@ struct OrientedView {
 int k5_oriented(const smg_graph& g, Replica& r, uint32_t shard, uint32_t num_shards, unsigned long long* count,
                 unsigned long long* units, double* ms) {
   if (!g_k4 || !g_relabel) return kTryGeneric;
+  SMG_CUDA(cudaSetDevice(r.device));
   int rc = ensure_oriented(g, r);
   if (rc) return rc;
   OrientedView view(r);
@@ -3063,6 +3064,7 @@ struct M4Out {
 int m4_count(const smg_graph& g, Replica& r, const int* kinds, const smg_plan* const* plans, uint32_t np,
              const Launch& L, M4Out* out) {
   r.post_kind = 0;
+  SMG_CUDA(cudaSetDevice(r.device));  // one host thread per device (m4_count_devices): set it here
   if (np == 1 && kinds[0] == kFastClique5) {
     unsigned long long c5 = 0, u5 = 0;
     double ms5 = 0;
