@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -126,14 +127,31 @@ int bits_for(uint64_t n) {
   return b;
 }
 
-struct Guard {  // frees temporaries on every exit path
+// Temporaries of one build, freed on every exit path.  Stream-ordered
+// allocations from the device's default pool, whose release threshold is
+// raised once so that the sort buffers of one call serve the next (a graph
+// handle per call pays no cudaMalloc/cudaFree round trips for them).
+struct Guard {
+  cudaStream_t st;
   std::vector<void*> ptrs;
+  explicit Guard(cudaStream_t s) : st(s) {
+    static std::once_flag once[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64)
+      std::call_once(once[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          unsigned long long keep = 8ull << 30;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+      });
+  }
   ~Guard() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, st);
   }
   template <class T>
   cudaError_t alloc(T** p, size_t bytes) {
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes ? bytes : 8);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 8, st);
     if (e == cudaSuccess) ptrs.push_back(*p);
     return e;
   }
@@ -151,7 +169,7 @@ struct Guard {  // frees temporaries on every exit path
 // Sort directed slot keys (2*mu or slots of them) into a CSR at `out`.
 int keys_to_csr(cudaStream_t st, unsigned long long* keys, unsigned long long* tmp, uint64_t slots,
                 uint64_t n, int num_sms, DevCSR* out, std::string* err) {
-  Guard g;
+  Guard g(st);
   const int end_bit = 32 + bits_for(n);
   size_t tb = 0;
   GB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, tmp, slots, 0, end_bit, st));
@@ -189,8 +207,8 @@ int keys_to_csr(cudaStream_t st, unsigned long long* keys, unsigned long long* t
 
 int device_from_edges(int dev, cudaStream_t st, int num_sms, const uint32_t* h_pairs, uint64_t m,
                       uint64_t n, DevCSR* out, uint64_t* dups, uint64_t* loops, std::string* err) {
-  Guard g;
   GB_CUDA(cudaSetDevice(dev));
+  Guard g(st);
   uint32_t* pairs = nullptr;
   unsigned long long *keys = nullptr, *sorted = nullptr, *counters = nullptr;
   unsigned int* bad = nullptr;
@@ -241,8 +259,8 @@ int device_from_edges(int dev, cudaStream_t st, int num_sms, const uint32_t* h_p
 
 int device_orient(int dev, cudaStream_t st, int num_sms, const DevCSR& in, DevCSR* out,
                   uint32_t* h_new_to_old, std::string* err) {
-  Guard g;
   GB_CUDA(cudaSetDevice(dev));
+  Guard g(st);
   const uint64_t n = in.n;
   unsigned long long *vkeys = nullptr, *vsorted = nullptr;
   uint32_t *n2o = nullptr, *o2n = nullptr;
